@@ -1,0 +1,226 @@
+// chain.cuh -- K1: fused 4-stage RK4 step for 1-D radius-1 models on two fields.
+//
+// Replaces one call of integrate_step (rk4.cpp:30-76) on the embedding
+// (system_model.cpp:56-77) of traffic (models.cpp:47-90) or the coupled chain
+// (SURVEY.md 8d C4), or on the growth-bound pair [center | radius]
+// (reach.cpp:103-114).  One CTA owns a tile of T components of BOTH fields
+// (so coupled decompositions read the other field in shared memory), loads it
+// with a halo of 4 (one per RK stage), runs the four stages in shared memory
+// and writes the tile once: 16 B of HBM traffic per state-update instead of
+// the reference's 144 B.
+//
+// Per-component arithmetic is exactly integrate_step's in exact mode:
+//   k0 = f(x); u1 = x + h2*k0; k1 = f(u1); u2 = x + h2*k1; k2 = f(u2);
+//   u3 = x + hk*k2; k3 = f(u3); x' = x + h6*(((k0 + 2k1) + 2k2) + k3).
+#pragma once
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace pirk {
+
+constexpr int kChainThreads = 256;
+constexpr int kChainPerThread = 4;
+constexpr int kChainSpan = kChainThreads * kChainPerThread;  // loaded elements per tile
+constexpr int kChainHalo = 4;
+constexpr int kChainTile = kChainSpan - 2 * kChainHalo;      // outputs per tile
+
+enum { kKindTraffic = 3, kKindChain = 5 };
+enum { kMethodMM = 0, kMethodGB = 1 };
+
+// traffic flux (models.cpp:59-61): min(c, min(v*from, w*(xbar-into)/beta)).
+template <bool Exact>
+__device__ __forceinline__ double traffic_flux(const ChainModel& m, double from, double into) {
+    const double v = m.P[0], w = m.P[1], c = m.P[2], xbar = m.P[3], beta = m.P[5];
+    if constexpr (Exact) {
+        return ref_min(c, ref_min(v * from, w * (xbar - into) / beta));
+    } else {
+        return ref_min(c, ref_min(v * from, m.wb * (xbar - into)));
+    }
+}
+
+// s(z) = z / (1 + |z|) for the coupled chain.
+__device__ __forceinline__ double chain_sat(double z) { return z / (1.0 + fabs(z)); }
+
+template <bool Exact, int Kind, int Method>
+__global__ void __launch_bounds__(kChainThreads)
+chain_step_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc,
+                  const unsigned long long step, unsigned long long* __restrict__ fail) {
+    (void)sizeof(ModeCheck<Exact>);
+    __shared__ double sU[2][2][kChainSpan];   // [buffer][field][j] stage input ping-pong
+    __shared__ double sA[2][kChainSpan];      // [field][j] per-stage auxiliary (edge flux / s(u))
+
+    const int tid = threadIdx.x;
+    const uint64_t n = m.n;
+    const long long o0 = static_cast<long long>(w.out_begin) +
+                         static_cast<long long>(blockIdx.x) * kChainTile;
+    const long long base = o0 - kChainHalo;  // global index of local j = 0
+
+    double x0[kChainPerThread], x1[kChainPerThread];
+    double acc0[kChainPerThread], acc1[kChainPerThread];
+
+    // ---- load the tile (+halo) of both fields; positions outside the window are NaN
+#pragma unroll
+    for (int r = 0; r < kChainPerThread; ++r) {
+        const int j = tid + r * kChainThreads;
+        const long long g = base + j;
+        double a = __longlong_as_double(0x7ff8000000000000ll), b = a;
+        if (g >= static_cast<long long>(w.win_begin) && g < static_cast<long long>(w.win_end)) {
+            a = w.in0[g - static_cast<long long>(w.win_begin)];
+            b = w.in1[g - static_cast<long long>(w.win_begin)];
+        }
+        x0[r] = a;
+        x1[r] = b;
+        sU[0][0][j] = a;
+        sU[0][1][j] = b;
+        acc0[r] = 0.0;
+        acc1[r] = 0.0;
+    }
+    __syncthreads();
+
+    int cur = 0;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        const double* u0 = sU[cur][0];
+        const double* u1 = sU[cur][1];
+
+        // ---- phase A: per-element / per-edge precompute over [s, span - s)
+        if constexpr (Kind == kKindTraffic) {
+#pragma unroll
+            for (int r = 0; r < kChainPerThread; ++r) {
+                const int j = tid + r * kChainThreads;
+                if (j >= s && j < kChainSpan - 1 - s) {
+                    sA[0][j] = traffic_flux<Exact>(m, u0[j], u0[j + 1]);  // edge j -> j+1
+                    if constexpr (Method == kMethodMM)
+                        sA[1][j] = traffic_flux<Exact>(m, u1[j], u1[j + 1]);
+                }
+            }
+            __syncthreads();
+        } else if constexpr (Kind == kKindChain) {
+#pragma unroll
+            for (int r = 0; r < kChainPerThread; ++r) {
+                const int j = tid + r * kChainThreads;
+                if (j >= s && j < kChainSpan - s) {
+                    sA[0][j] = chain_sat(u0[j]);
+                    sA[1][j] = chain_sat(u1[j]);
+                }
+            }
+            __syncthreads();
+        }
+
+        // ---- phase B: stage derivative and update over [s+1, span-1-s)
+        double* n0 = sU[cur ^ 1][0];
+        double* n1 = sU[cur ^ 1][1];
+#pragma unroll
+        for (int r = 0; r < kChainPerThread; ++r) {
+            const int j = tid + r * kChainThreads;
+            const long long g = base + j;
+            if (j < s + 1 || j >= kChainSpan - 1 - s) continue;
+            if (g < 0 || g >= static_cast<long long>(n)) continue;
+            const bool first = (g == 0);
+            const bool last = (g + 1 == static_cast<long long>(n));
+            double k0v, k1v;
+            if constexpr (Kind == kKindTraffic) {
+                const double v = m.P[0], c = m.P[2], beta = m.P[5];
+                // models.cpp:68-74 with the flux of each edge shared by its two
+                // end components (same inputs, hence bit-identical).
+                {
+                    const double in = first ? beta * m.p0 : beta * sA[0][j - 1];
+                    const double out = last ? ref_min(c, v * u0[j]) : sA[0][j];
+                    k0v = m.inv_t * (in - out);
+                }
+                if constexpr (Method == kMethodMM) {
+                    const double in = first ? beta * m.p1 : beta * sA[1][j - 1];
+                    const double out = last ? ref_min(c, v * u1[j]) : sA[1][j];
+                    k1v = m.inv_t * (in - out);
+                } else {
+                    // growth_rhs, models.cpp:78-87
+                    double gv = first ? m.a_in * m.p1 : m.a_prev * u1[j - 1];
+                    if (!last) gv += m.a_next * u1[j + 1];
+                    k1v = gv;
+                }
+            } else {  // coupled chain: d_i(x,p,xh,ph) = ((-a) x_i + b s(x_{i-1}) - c s(xh_{i+1})) + p
+                const double na = -m.P[0], b = m.P[1], c = m.P[2];
+                {
+                    const double sl = first ? 0.0 : sA[0][j - 1];
+                    const double sr = last ? 0.0 : sA[1][j + 1];
+                    k0v = (na * u0[j] + b * sl - c * sr) + m.p0;
+                }
+                {
+                    const double sl = first ? 0.0 : sA[1][j - 1];
+                    const double sr = last ? 0.0 : sA[0][j + 1];
+                    k1v = (na * u1[j] + b * sl - c * sr) + m.p1;
+                }
+            }
+            if (s == 0) {
+                acc0[r] = k0v;
+                acc1[r] = k1v;
+                n0[j] = x0[r] + sc.h2 * k0v;
+                n1[j] = x1[r] + sc.h2 * k1v;
+            } else if (s == 1) {
+                acc0[r] = acc0[r] + 2.0 * k0v;
+                acc1[r] = acc1[r] + 2.0 * k1v;
+                n0[j] = x0[r] + sc.h2 * k0v;
+                n1[j] = x1[r] + sc.h2 * k1v;
+            } else if (s == 2) {
+                acc0[r] = acc0[r] + 2.0 * k0v;
+                acc1[r] = acc1[r] + 2.0 * k1v;
+                n0[j] = x0[r] + sc.hk * k0v;
+                n1[j] = x1[r] + sc.hk * k1v;
+            } else {
+                // final update; j in [4, span-4) here, i.e. the tile's own outputs
+                x0[r] = x0[r] + sc.h6 * (acc0[r] + k0v);
+                x1[r] = x1[r] + sc.h6 * (acc1[r] + k1v);
+            }
+        }
+        if (s < 3) __syncthreads();
+        cur ^= 1;
+    }
+
+    // ---- store the tile's outputs and flag non-finite values
+#pragma unroll
+    for (int r = 0; r < kChainPerThread; ++r) {
+        const int j = tid + r * kChainThreads;
+        const long long g = base + j;
+        if (j < kChainHalo || j >= kChainSpan - kChainHalo) continue;
+        if (g < static_cast<long long>(w.out_begin) || g >= static_cast<long long>(w.out_end))
+            continue;
+        const long long o = g - static_cast<long long>(w.out_begin);
+        w.out0[o] = x0[r];
+        w.out1[o] = x1[r];
+        if (!finite_d(x0[r]) || !finite_d(x1[r])) {
+            if constexpr (Method == kMethodMM) {
+                // embedding components are numbered [x | xh] (system_model.cpp:67-75)
+                const unsigned long long comp =
+                    finite_d(x0[r]) ? static_cast<unsigned long long>(g) + n
+                                    : static_cast<unsigned long long>(g);
+                record_fail(fail, step, comp);
+            } else {
+                if (!finite_d(x0[r])) record_fail(fail, step, static_cast<unsigned long long>(g));
+                if (!finite_d(x1[r]) && fail)
+                    record_fail(fail + 1, step, static_cast<unsigned long long>(g));
+            }
+        }
+    }
+}
+
+template <bool Exact>
+cudaError_t launch_chain_step(const ChainModel& m, const WindowArgs& w, const StepConsts& sc,
+                              unsigned long long step, unsigned long long* fail,
+                              cudaStream_t stream) {
+    if (w.out_end <= w.out_begin) return cudaSuccess;
+    const uint64_t count = w.out_end - w.out_begin;
+    const unsigned int blocks = static_cast<unsigned int>((count + kChainTile - 1) / kChainTile);
+    dim3 grid(blocks), block(kChainThreads);
+    if (m.kind == kKindTraffic && m.method == kMethodMM)
+        chain_step_kernel<Exact, kKindTraffic, kMethodMM><<<grid, block, 0, stream>>>(m, w, sc, step, fail);
+    else if (m.kind == kKindTraffic && m.method == kMethodGB)
+        chain_step_kernel<Exact, kKindTraffic, kMethodGB><<<grid, block, 0, stream>>>(m, w, sc, step, fail);
+    else if (m.kind == kKindChain && m.method == kMethodMM)
+        chain_step_kernel<Exact, kKindChain, kMethodMM><<<grid, block, 0, stream>>>(m, w, sc, step, fail);
+    else
+        return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+}  // namespace pirk

@@ -1,0 +1,1128 @@
+// engine.cu -- host side of the C ABI (include/pirk_c.h).
+//
+// Restates the reference's method drivers (reach.cpp:65-323) around device
+// kernels: validation (system_model.cpp:10-32, interval.cpp:10-23), step
+// planning (rk4.cpp:8-17, reach.cpp:28-39), the step loop with last-step
+// shortening (rk4.cpp:98-112), recording, and the error contract (messages
+// and priorities of reach.cpp:107-117, 181-192, 306-312).  All arithmetic on
+// the state runs in the device kernels; the host only plans, launches,
+// transfers and formats.  There is no CPU fallback: an unsupported model or
+// a missing device is an error.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#define PIRK_TU_EXACT 1
+#include "../../include/pirk_c.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace pirk;
+
+struct pirk_ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    int mode = PIRK_MODE_EXACT;
+    std::string err;
+    uint64_t launches = 0;
+    unsigned long long* d_flags = nullptr;  // scratch device flags [16]
+    unsigned long long* h_flags = nullptr;  // pinned mirror
+};
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double since(Clock::time_point t) { return std::chrono::duration<double>(Clock::now() - t).count(); }
+
+pirk_status fail(pirk_ctx* ctx, pirk_status st, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return st;
+}
+
+pirk_status cuda_fail(pirk_ctx* ctx, cudaError_t e, const char* what) {
+    const pirk_status st = (e == cudaErrorMemoryAllocation) ? PIRK_ENOMEM : PIRK_ECUDA;
+    if (e == cudaErrorMemoryAllocation) cudaGetLastError();  // clear the sticky-free error
+    return fail(ctx, st, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(ctx, expr)                                                  \
+    do {                                                               \
+        cudaError_t e_ = (expr);                                       \
+        if (e_ != cudaSuccess) return cuda_fail((ctx), e_, #expr);     \
+    } while (0)
+
+// std::to_string(double) == "%f" (the reference formats t and radii this way)
+std::string fstr(double v) {
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%f", v);
+    return buf;
+}
+
+struct Plan {
+    uint64_t full = 0, total = 0;
+    bool rem = false;
+};
+
+// rk4.cpp:8-17
+bool plan_steps(double t0, double t1, double h, Plan& p) {
+    if (!(h > 0.0) || !(t0 < t1)) return false;
+    const double span = t1 - t0;
+    p.full = static_cast<uint64_t>(std::floor(span / h + 1e-9));
+    const double remainder = span - static_cast<double>(p.full) * h;
+    p.rem = remainder > 1e-9 * h;
+    p.total = p.full + (p.rem ? 1 : 0);
+    return true;
+}
+
+// reach.cpp:28-39
+void record_schedule(double t0, double t1, double h, uint64_t stride, const Plan& plan,
+                     std::vector<uint64_t>& steps, std::vector<double>& times) {
+    steps.clear();
+    times.clear();
+    if (stride > 0) {
+        steps.push_back(0);
+        times.push_back(t0);
+        for (uint64_t k = stride; k < plan.total; k += stride) {
+            steps.push_back(k);
+            times.push_back(t0 + static_cast<double>(k) * h);
+        }
+    }
+    steps.push_back(plan.total);
+    times.push_back(t1);
+}
+
+// rk4.cpp:99-100, 38-39
+StepConsts host_step(double t0, double t1, double h, uint64_t k, uint64_t total) {
+    StepConsts c;
+    c.t = t0 + static_cast<double>(k) * h;
+    c.hk = (k + 1 == total) ? t1 - c.t : h;
+    c.h2 = 0.5 * c.hk;
+    c.h6 = c.hk / 6.0;
+    return c;
+}
+
+bool is_chain(const pirk_model* m) { return m->kind == PIRK_TRAFFIC || m->kind == PIRK_CHAIN; }
+bool is_heat(const pirk_model* m) { return m->kind == PIRK_HEAT3D; }
+
+// Descriptor consistency (the reference's make_* constructors enforce these,
+// models.cpp:47-53, 92-97, and fix dim/input_dim per model).
+bool check_model(pirk_ctx* ctx, const pirk_model* m, pirk_status& st) {
+    auto bad = [&](const std::string& s) {
+        st = fail(ctx, PIRK_EINVAL, "model descriptor: " + s);
+        return false;
+    };
+    if (!m) return bad("null model");
+    if (m->dim == 0) {
+        st = fail(ctx, PIRK_EINVAL, "problem: model has no dynamics");
+        return false;
+    }
+    switch (m->kind) {
+        case PIRK_ZERO:
+            if (m->input_dim != 0) return bad("zero model has no inputs");
+            break;
+        case PIRK_SCALAR_DECAY:
+            if (m->dim != 1 || m->input_dim != 1) return bad("scalar-decay is 1-D with 1 input");
+            break;
+        case PIRK_SCALAR_LINEAR:
+            if (m->dim != 1 || m->input_dim != 0) return bad("scalar-linear is 1-D without inputs");
+            break;
+        case PIRK_TRAFFIC:
+            if (m->dim < 3) return bad("traffic model needs at least 3 segments");
+            if (m->input_dim != 1) return bad("traffic has one input");
+            break;
+        case PIRK_HEAT3D:
+            if (m->grid < 2 || m->grid * m->grid * m->grid != m->dim)
+                return bad("heat3d needs grid >= 2 and dim == grid^3");
+            if (m->input_dim != 0) return bad("heat3d has no inputs");
+            break;
+        case PIRK_CHAIN:
+            if (m->input_dim != 1) return bad("chain has one input");
+            break;
+        case PIRK_LAUB_LOOMIS:
+            if (m->dim != 7 || m->input_dim != 0) return bad("laub-loomis is 7-D without inputs");
+            break;
+        case PIRK_ARCH_QUAD:
+            if (m->dim != 12 || m->input_dim != 0) return bad("arch-quadrotor is 12-D without inputs");
+            break;
+        case PIRK_VDP:
+            if (m->dim != 2 || m->input_dim != 0) return bad("vdp is 2-D without inputs");
+            break;
+        default:
+            return bad("unknown model kind " + std::to_string(m->kind));
+    }
+    if (m->decomp < PIRK_DECOMP_NONE || m->decomp > PIRK_DECOMP_JACOBIAN)
+        return bad("unknown decomposition");
+    return true;
+}
+
+// Dense growth matrices (models.cpp:457-460, 488-500, 557-611), computed with
+// the host libm exactly as the reference constructs them.
+bool growth_matrix(const pirk_model* m, double* C) {
+    const uint64_t n = m->dim;
+    std::memset(C, 0, sizeof(double) * 144);
+    if (m->kind == PIRK_VDP) {
+        const double mu = m->params[0], op_x = m->params[1], op_y = m->params[2];
+        C[0 * 2 + 1] = 1.0;
+        C[1 * 2 + 0] = 2.0 * mu * op_x * op_y + 1.0;
+        C[1 * 2 + 1] = mu;
+        return true;
+    }
+    if (m->kind == PIRK_LAUB_LOOMIS) {
+        const double xm = 5.0;
+        const double rows[7][7] = {
+            {-0.9, 0, 1.4, 0, 0, 0, 0},     {0, -1.5, 0, 0, 2.5, 0, 0},
+            {0, 0.8 * xm, 0, 0, 0, 0, 0.6}, {0, 0, 1.3 * xm, 0, 0, 0, 0},
+            {0.7, 0, 0, xm, 0, 0, 0},       {0.3, 0, 0, 0, 0, -3.1, 0},
+            {0, 1.5 * xm, 0, 0, 0, 1.8, 0},
+        };
+        for (uint64_t i = 0; i < 7; ++i)
+            for (uint64_t j = 0; j < 7; ++j) C[i * n + j] = rows[i][j];
+        return true;
+    }
+    if (m->kind == PIRK_ARCH_QUAD) {
+        const double mass = m->params[0], gravity = m->params[1];
+        const double jx = m->params[2], jy = m->params[3], jz = m->params[4];
+        const double kx = (jy - jz) / jx, ky = (jz - jx) / jy, kz = (jx - jy) / jz;
+        const double vb = 5.0, ab = 0.5, rb = 2.0;
+        const double tanb = std::tan(ab);
+        const double secb = 1.0 / std::cos(ab);
+        const double sec2b = secb * secb;
+        const double akx = std::fabs(kx), aky = std::fabs(ky), akz = std::fabs(kz);
+        auto c = [&](int r, int col) -> double& { return C[r * 12 + col]; };
+        for (int row = 0; row < 3; ++row) {
+            c(row, 3) = c(row, 4) = c(row, 5) = 1.0;
+            c(row, 6) = c(row, 7) = 6.0 * vb;
+            if (row < 2) c(row, 8) = 6.0 * vb;
+        }
+        c(3, 4) = rb; c(3, 5) = rb; c(3, 7) = gravity; c(3, 10) = vb; c(3, 11) = vb;
+        c(4, 3) = rb; c(4, 5) = rb; c(4, 6) = gravity; c(4, 7) = gravity; c(4, 9) = vb; c(4, 11) = vb;
+        c(5, 2) = 10.0 / mass; c(5, 3) = rb; c(5, 4) = rb; c(5, 5) = -3.0 / mass;
+        c(5, 6) = gravity; c(5, 7) = gravity; c(5, 9) = vb; c(5, 10) = vb;
+        c(6, 6) = 2.0 * tanb * rb; c(6, 7) = 2.0 * sec2b * rb; c(6, 9) = 1.0;
+        c(6, 10) = tanb; c(6, 11) = tanb;
+        c(7, 6) = 2.0 * rb; c(7, 10) = 1.0; c(7, 11) = 1.0;
+        c(8, 6) = 2.0 * secb * rb; c(8, 7) = 2.0 * secb * tanb * rb; c(8, 10) = secb; c(8, 11) = secb;
+        c(9, 6) = 1.0 / jx; c(9, 9) = -1.0 / jx; c(9, 10) = akx * rb; c(9, 11) = akx * rb;
+        c(10, 7) = 1.0 / jy; c(10, 9) = aky * rb; c(10, 10) = -1.0 / jy; c(10, 11) = aky * rb;
+        c(11, 9) = akz * rb; c(11, 10) = akz * rb;
+        return true;
+    }
+    return false;
+}
+
+bool has_growth(const pirk_model* m) {
+    return m->kind == PIRK_ZERO || m->kind == PIRK_SCALAR_DECAY || m->kind == PIRK_SCALAR_LINEAR ||
+           m->kind == PIRK_TRAFFIC || m->kind == PIRK_HEAT3D || m->kind == PIRK_LAUB_LOOMIS ||
+           m->kind == PIRK_ARCH_QUAD || m->kind == PIRK_VDP;
+}
+
+SmallModel small_model(const pirk_model* m) {
+    SmallModel s{};
+    s.kind = m->kind;
+    s.decomp = m->decomp;
+    s.n = static_cast<int>(m->dim);
+    s.ni = static_cast<int>(m->input_dim);
+    s.grid = m->grid;
+    for (int i = 0; i < 8; ++i) s.P[i] = m->params[i];
+    s.has_C = growth_matrix(m, s.C) ? 1 : 0;
+    return s;
+}
+
+ChainModel chain_model(const pirk_model* m, int method, double p0, double p1) {
+    ChainModel c{};
+    c.kind = m->kind;
+    c.method = method;
+    c.n = m->dim;
+    for (int i = 0; i < 8; ++i) c.P[i] = m->params[i];
+    c.p0 = p0;
+    c.p1 = p1;
+    if (m->kind == PIRK_TRAFFIC) {  // models.cpp:55, 79-81
+        const double v = m->params[0], w = m->params[1], beta = m->params[5];
+        c.inv_t = 1.0 / m->params[4];
+        c.a_prev = beta * v * c.inv_t;
+        c.a_next = (w / beta) * c.inv_t;
+        c.a_in = beta * c.inv_t;
+        c.wb = w / beta;
+    }
+    return c;
+}
+
+HeatModel heat_model(const pirk_model* m, int method) {
+    HeatModel h{};  // models.cpp:99-101
+    h.method = method;
+    h.g = m->grid;
+    const double delta = 1.0 / static_cast<double>(m->grid - 1);
+    h.kk = m->params[0] / (delta * delta);
+    h.robin = 2.0 * delta * m->params[1];
+    return h;
+}
+
+bool small_ok(const pirk_model* m) { return m->dim <= static_cast<uint64_t>(kSmallMax); }
+
+// Problem validation (system_model.cpp:10-32) except the per-component box
+// checks of large models, which run on the device after upload.
+bool check_problem(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p, bool host_box,
+                   pirk_status& st) {
+    if (!check_model(ctx, m, st)) return false;
+    if (!p || !p->init_lower || !p->init_upper) {
+        st = fail(ctx, PIRK_EINVAL, "problem: initial box missing");
+        return false;
+    }
+    if (host_box) {
+        for (uint64_t i = 0; i < m->dim; ++i) {
+            if (!std::isfinite(p->init_lower[i]) || !std::isfinite(p->init_upper[i])) {
+                st = fail(ctx, PIRK_EINVAL, "interval: non-finite bound at component " + std::to_string(i));
+                return false;
+            }
+            if (p->init_lower[i] > p->init_upper[i]) {
+                st = fail(ctx, PIRK_EINVAL, "interval: lower > upper at component " + std::to_string(i));
+                return false;
+            }
+        }
+    }
+    if (m->input_dim == 0) {
+        if (p->input_lower || p->input_upper) {
+            st = fail(ctx, PIRK_EINVAL, "problem: model has no inputs but an input box was given");
+            return false;
+        }
+    } else {
+        if (!p->input_lower || !p->input_upper) {
+            st = fail(ctx, PIRK_EINVAL, "problem: model has " + std::to_string(m->input_dim) +
+                                            " inputs but no input box was given");
+            return false;
+        }
+        for (uint64_t j = 0; j < m->input_dim; ++j) {
+            if (!std::isfinite(p->input_lower[j]) || !std::isfinite(p->input_upper[j])) {
+                st = fail(ctx, PIRK_EINVAL, "interval: non-finite bound at component " + std::to_string(j));
+                return false;
+            }
+            if (p->input_lower[j] > p->input_upper[j]) {
+                st = fail(ctx, PIRK_EINVAL, "interval: lower > upper at component " + std::to_string(j));
+                return false;
+            }
+        }
+    }
+    if (!(p->t0 < p->t1)) {
+        st = fail(ctx, PIRK_EINVAL, "problem: t0 must be earlier than t1");
+        return false;
+    }
+    if (!(p->h > 0.0)) {
+        st = fail(ctx, PIRK_EINVAL, "problem: step size h must be positive");
+        return false;
+    }
+    return true;
+}
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    ~DevBuf() { if (p) cudaFree(p); }
+    cudaError_t alloc(size_t count) { return cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T) + 16); }
+};
+
+bool exact_mode(const pirk_ctx* ctx) { return ctx->mode == PIRK_MODE_EXACT; }
+
+cudaError_t step_launch(pirk_ctx* ctx, const pirk_model* m, int method, const ChainModel& cm,
+                        const HeatModel& hm, const WindowArgs& w, const StepConsts& sc,
+                        uint64_t k, unsigned long long* fail_ptr) {
+    ctx->launches++;
+    const bool ex = exact_mode(ctx);
+    (void)method;
+    if (is_chain(m))
+        return ex ? launch_chain_step<true>(cm, w, sc, k, fail_ptr, ctx->stream)
+                  : launch_chain_step<false>(cm, w, sc, k, fail_ptr, ctx->stream);
+    return ex ? launch_heat_step<true>(hm, w, sc, k, fail_ptr, ctx->stream)
+              : launch_heat_step<false>(hm, w, sc, k, fail_ptr, ctx->stream);
+}
+
+std::string integ_msg(uint64_t step, uint64_t comp, double t) {
+    return "integration produced a non-finite value at step " + std::to_string(step) +
+           ", component " + std::to_string(comp) + ", t = " + fstr(t);
+}
+
+void fill_report(pirk_report* r, uint64_t n, uint64_t m, uint64_t steps, uint64_t peak,
+                 uint64_t dev_bytes, bool exact, double setup, double integ, double red,
+                 uint64_t launches) {
+    if (!r) return;
+    r->n = n;
+    r->m = m;
+    r->steps = steps;
+    r->peak_state_bytes = peak;
+    r->device_state_bytes = dev_bytes;
+    r->workers = 1;
+    r->exact = exact ? 1 : 0;
+    r->setup_s = setup;
+    r->integration_s = integ;
+    r->reduction_s = red;
+    r->kernel_launches = launches;
+}
+
+}  // namespace
+
+// ============================================================= engine object
+
+struct pirk_engine {
+    pirk_ctx* ctx = nullptr;
+    pirk_model model{};
+    int method = 0;
+    Plan plan;
+    double t0 = 0, t1 = 0, h = 0;
+    uint64_t n = 0, units = 0, unit = 1;
+    DevBuf<double> a0, a1, b0, b1;
+    int cur = 0;               // 0: state in (a0,a1); 1: in (b0,b1)
+    uint64_t done = 0;
+    DevBuf<unsigned long long> d_fail;  // [2]
+    ChainModel cm{};
+    HeatModel hm{};
+    double* s0() { return cur ? b0.p : a0.p; }
+    double* s1() { return cur ? b1.p : a1.p; }
+    double* o0() { return cur ? a0.p : b0.p; }
+    double* o1() { return cur ? a1.p : b1.p; }
+};
+
+namespace {
+
+pirk_status engine_init(pirk_ctx* ctx, const pirk_model* m, int method, const pirk_problem* p,
+                        pirk_engine* e) {
+    e->ctx = ctx;
+    e->model = *m;
+    e->method = method;
+    e->t0 = p->t0;
+    e->t1 = p->t1;
+    e->h = p->h;
+    plan_steps(p->t0, p->t1, p->h, e->plan);
+    if (e->plan.total >= (1ull << 23))
+        return fail(ctx, PIRK_EINVAL, "step count exceeds the device failure-key range (2^23)");
+    e->n = m->dim;
+    e->unit = is_heat(m) ? m->grid * m->grid : 1;
+    e->units = e->n / e->unit;
+    if (2 * e->n >= (1ull << kFailCompBits))
+        return fail(ctx, PIRK_EINVAL, "dimension exceeds the device failure-key range");
+    double p0 = 0.0, p1 = 0.0;
+    if (m->input_dim > 0) {
+        if (method == PIRK_METHOD_MM) {
+            p0 = p->input_lower[0];
+            p1 = p->input_upper[0];
+        } else {  // interval.cpp:25-37 center / half-width
+            p0 = 0.5 * (p->input_upper[0] + p->input_lower[0]);
+            p1 = 0.5 * (p->input_upper[0] - p->input_lower[0]);
+        }
+    }
+    e->cm = chain_model(m, method, p0, p1);
+    e->hm = heat_model(m, method);
+    const size_t n = e->n;
+    CK(ctx, e->a0.alloc(n));
+    CK(ctx, e->a1.alloc(n));
+    CK(ctx, e->b0.alloc(n));
+    CK(ctx, e->b1.alloc(n));
+    CK(ctx, e->d_fail.alloc(2));
+    CK(ctx, cudaMemsetAsync(e->d_fail.p, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
+    CK(ctx, cudaMemcpyAsync(e->a0.p, p->init_lower, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(ctx, cudaMemcpyAsync(e->a1.p, p->init_upper, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    // IntervalVector validation of the uploaded box, on the device
+    CK(ctx, cudaMemsetAsync(ctx->d_flags, 0xff, sizeof(unsigned long long), ctx->stream));
+    CK(ctx, launch_box_check(e->a0.p, e->a1.p, n, ctx->d_flags, ctx->stream));
+    ctx->launches++;
+    CK(ctx, cudaMemcpyAsync(ctx->h_flags, ctx->d_flags, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (ctx->h_flags[0] != kNoFail) {
+        const uint64_t i = ctx->h_flags[0];
+        const bool nonfinite = !std::isfinite(p->init_lower[i]) || !std::isfinite(p->init_upper[i]);
+        return fail(ctx, PIRK_EINVAL, std::string(nonfinite ? "interval: non-finite bound at component "
+                                                            : "interval: lower > upper at component ") +
+                                          std::to_string(i));
+    }
+    if (method == PIRK_METHOD_GB) {
+        CK(ctx, launch_center_radius(e->a0.p, e->a1.p, n, ctx->stream));
+        ctx->launches++;
+    }
+    e->cur = 0;
+    e->done = 0;
+    return PIRK_OK;
+}
+
+pirk_status engine_advance(pirk_engine* e, uint64_t nsteps) {
+    pirk_ctx* ctx = e->ctx;
+    for (uint64_t i = 0; i < nsteps && e->done < e->plan.total; ++i) {
+        const uint64_t k = e->done;
+        const StepConsts sc = host_step(e->t0, e->t1, e->h, k, e->plan.total);
+        WindowArgs w{e->s0(), e->s1(), e->o0(), e->o1(), 0, e->units, 0, e->units};
+        CK(ctx, step_launch(ctx, &e->model, e->method, e->cm, e->hm, w, sc, k, e->d_fail.p));
+        e->cur ^= 1;
+        e->done++;
+    }
+    return PIRK_OK;
+}
+
+// Large-model (chain / heat kernels) MM and GB driver.
+pirk_status run_large(pirk_ctx* ctx, const pirk_model* m, int method, const pirk_problem* p,
+                      pirk_tube* tube, pirk_report* rep) {
+    const auto t_setup = Clock::now();
+    const uint64_t launches0 = ctx->launches;
+    pirk_engine e;
+    pirk_status st = engine_init(ctx, m, method, p, &e);
+    if (st != PIRK_OK) return st;
+    std::vector<uint64_t> slot_steps;
+    std::vector<double> slot_times;
+    record_schedule(p->t0, p->t1, p->h, p->tube_stride, e.plan, slot_steps, slot_times);
+    const uint64_t S = slot_steps.size();
+    if (tube && tube->max_slots < S)
+        return fail(ctx, PIRK_EINVAL, "tube: max_slots " + std::to_string(tube->max_slots) +
+                                          " < record slots " + std::to_string(S));
+    DevBuf<unsigned long long> slot_flag;  // per slot: order (MM) / negative radius (GB)
+    DevBuf<double> slot_val;
+    CK(ctx, slot_flag.alloc(S));
+    CK(ctx, slot_val.alloc(S));
+    CK(ctx, cudaMemsetAsync(slot_flag.p, 0xff, S * sizeof(unsigned long long), ctx->stream));
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    const double setup_s = since(t_setup);
+
+    const auto t_int = Clock::now();
+    const uint64_t n = e.n;
+    for (uint64_t s = 0; s < S; ++s) {
+        st = engine_advance(&e, slot_steps[s] - e.done);
+        if (st != PIRK_OK) return st;
+        const double* out_lo = e.s0();
+        const double* out_hi = e.s1();
+        if (method == PIRK_METHOD_MM) {
+            CK(ctx, launch_order_check(e.s0(), e.s1(), n, slot_flag.p + s, ctx->stream));
+        } else {
+            // the free ping-pong buffers receive the clamped box
+            CK(ctx, launch_gb_box(e.s0(), e.s1(), e.o0(), e.o1(), n, slot_flag.p + s, ctx->stream));
+            CK(ctx, launch_gb_negval(e.s1(), slot_flag.p + s, slot_val.p + s, ctx->stream));
+            ctx->launches++;
+            out_lo = e.o0();
+            out_hi = e.o1();
+        }
+        ctx->launches++;
+        if (tube && tube->lower)
+            CK(ctx, cudaMemcpyAsync(tube->lower + s * n, out_lo, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        if (tube && tube->upper)
+            CK(ctx, cudaMemcpyAsync(tube->upper + s * n, out_hi, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    std::vector<unsigned long long> flags(S);
+    std::vector<double> vals(S);
+    CK(ctx, cudaMemcpyAsync(ctx->h_flags, e.d_fail.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaMemcpyAsync(flags.data(), slot_flag.p, S * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaMemcpyAsync(vals.data(), slot_val.p, S * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    const double integ_s = since(t_int);
+
+    if (tube) {
+        tube->n_slots = S;
+        if (tube->times)
+            for (uint64_t s = 0; s < S; ++s) tube->times[s] = slot_times[s];
+    }
+    // ---- error contract, in the reference's order of detection
+    const unsigned long long f0 = ctx->h_flags[0], f1 = ctx->h_flags[1];
+    auto decode = [](unsigned long long key, uint64_t& step, uint64_t& comp) {
+        step = key >> kFailCompBits;
+        comp = key & ((1ull << kFailCompBits) - 1);
+    };
+    if (method == PIRK_METHOD_MM) {
+        uint64_t fs = 0, fc = 0;
+        if (f0 != kNoFail) decode(f0, fs, fc);
+        for (uint64_t s = 0; s < S; ++s) {
+            // an integration failure in step k is raised before slot k+1 is observed
+            if (f0 != kNoFail && fs < slot_steps[s])
+                return fail(ctx, PIRK_EINTEGRATION, "mixed-monotonicity embedding integration: " +
+                                                        integ_msg(fs, fc, p->t0 + static_cast<double>(fs) * p->h));
+            if (flags[s] != kNoFail)
+                return fail(ctx, PIRK_EORDER, "mixed-monotonicity: embedding order violated at step " +
+                                                  std::to_string(slot_steps[s]) + ", t = " + fstr(slot_times[s]) +
+                                                  ", component " + std::to_string(flags[s]));
+        }
+        if (f0 != kNoFail)
+            return fail(ctx, PIRK_EINTEGRATION, "mixed-monotonicity embedding integration: " +
+                                                    integ_msg(fs, fc, p->t0 + static_cast<double>(fs) * p->h));
+        fill_report(rep, n, 0, e.plan.total, 7 * 2 * n * sizeof(double), 4 * n * sizeof(double),
+                    exact_mode(ctx), setup_s, integ_s, 0.0, ctx->launches - launches0);
+    } else {
+        // center integration runs to completion before the radius integration
+        // (reach.cpp:103-117), and the clamp pass follows both (reach.cpp:121-134)
+        uint64_t fs = 0, fc = 0;
+        if (f0 != kNoFail) {
+            decode(f0, fs, fc);
+            return fail(ctx, PIRK_EINTEGRATION, "growth-bound center integration: " +
+                                                    integ_msg(fs, fc, p->t0 + static_cast<double>(fs) * p->h));
+        }
+        if (f1 != kNoFail) {
+            decode(f1, fs, fc);
+            return fail(ctx, PIRK_EINTEGRATION, "growth-bound radius integration: " +
+                                                    integ_msg(fs, fc, p->t0 + static_cast<double>(fs) * p->h));
+        }
+        for (uint64_t s = 0; s < S; ++s)
+            if (flags[s] != kNoFail)
+                return fail(ctx, PIRK_ENEGRADIUS, "growth-bound: deviation went negative (" + fstr(vals[s]) +
+                                                      ") at component " + std::to_string(flags[s]) +
+                                                      "; contraction matrix is invalid");
+        fill_report(rep, n, 0, e.plan.total, 7 * n * sizeof(double), 4 * n * sizeof(double),
+                    exact_mode(ctx), setup_s, integ_s, 0.0, ctx->launches - launches0);
+    }
+    return PIRK_OK;
+}
+
+// Small-model MM / GB: one device thread per integration.
+pirk_status run_small(pirk_ctx* ctx, const pirk_model* m, int method, const pirk_problem* p,
+                      pirk_tube* tube, pirk_report* rep) {
+    const auto t_setup = Clock::now();
+    const uint64_t launches0 = ctx->launches;
+    Plan plan;
+    plan_steps(p->t0, p->t1, p->h, plan);
+    std::vector<uint64_t> slot_steps;
+    std::vector<double> slot_times;
+    record_schedule(p->t0, p->t1, p->h, p->tube_stride, plan, slot_steps, slot_times);
+    const uint64_t S = slot_steps.size();
+    if (tube && tube->max_slots < S)
+        return fail(ctx, PIRK_EINVAL, "tube: max_slots too small");
+    const uint64_t n = m->dim, ni = m->input_dim;
+    const SmallModel sm = small_model(m);
+    const bool ex = exact_mode(ctx);
+    std::vector<double> host_rec0, host_rec1;
+    unsigned long long f0 = kNoFail, f1 = kNoFail;
+    double setup_s = 0.0;
+    const auto t_int = Clock::now();
+    if (method == PIRK_METHOD_MM) {
+        // x0 = [lower | upper], p = [p_lo | p_hi] (reach.cpp:150-161)
+        std::vector<double> x0(2 * n), pp(2 * ni + 1, 0.0);
+        for (uint64_t i = 0; i < n; ++i) { x0[i] = p->init_lower[i]; x0[n + i] = p->init_upper[i]; }
+        for (uint64_t j = 0; j < ni; ++j) { pp[j] = p->input_lower[j]; pp[ni + j] = p->input_upper[j]; }
+        DevBuf<double> dx, dp, drec;
+        DevBuf<unsigned long long> dfail;
+        CK(ctx, dx.alloc(2 * n));
+        CK(ctx, dp.alloc(pp.size()));
+        CK(ctx, drec.alloc(S * 2 * n));
+        CK(ctx, dfail.alloc(1));
+        CK(ctx, cudaMemcpyAsync(dx.p, x0.data(), 2 * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CK(ctx, cudaMemcpyAsync(dp.p, pp.data(), pp.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CK(ctx, cudaMemsetAsync(dfail.p, 0xff, sizeof(unsigned long long), ctx->stream));
+        setup_s = since(t_setup);
+        CK(ctx, ex ? launch_small_integrate<true>(sm, 2, dx.p, dp.p, p->t0, p->t1, p->h, plan.total, p->tube_stride, drec.p, dfail.p, ctx->stream)
+                   : launch_small_integrate<false>(sm, 2, dx.p, dp.p, p->t0, p->t1, p->h, plan.total, p->tube_stride, drec.p, dfail.p, ctx->stream));
+        ctx->launches++;
+        host_rec0.resize(S * 2 * n);
+        CK(ctx, cudaMemcpyAsync(host_rec0.data(), drec.p, S * 2 * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(ctx, cudaMemcpyAsync(&f0, dfail.p, sizeof f0, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(ctx, cudaStreamSynchronize(ctx->stream));
+    } else {
+        // center/radius of the initial and input boxes (interval.cpp:25-37)
+        std::vector<double> c0(n), r0(n), pc(ni + 1, 0.0), w(ni + 1, 0.0);
+        for (uint64_t i = 0; i < n; ++i) {
+            c0[i] = 0.5 * (p->init_upper[i] + p->init_lower[i]);
+            r0[i] = 0.5 * (p->init_upper[i] - p->init_lower[i]);
+        }
+        for (uint64_t j = 0; j < ni; ++j) {
+            pc[j] = 0.5 * (p->input_upper[j] + p->input_lower[j]);
+            w[j] = 0.5 * (p->input_upper[j] - p->input_lower[j]);
+        }
+        DevBuf<double> dc, dr, dpc, dw, drec0, drec1;
+        DevBuf<unsigned long long> dfail;
+        CK(ctx, dc.alloc(n)); CK(ctx, dr.alloc(n)); CK(ctx, dpc.alloc(ni + 1)); CK(ctx, dw.alloc(ni + 1));
+        CK(ctx, drec0.alloc(S * n)); CK(ctx, drec1.alloc(S * n)); CK(ctx, dfail.alloc(2));
+        CK(ctx, cudaMemcpyAsync(dc.p, c0.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CK(ctx, cudaMemcpyAsync(dr.p, r0.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CK(ctx, cudaMemcpyAsync(dpc.p, pc.data(), (ni + 1) * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CK(ctx, cudaMemcpyAsync(dw.p, w.data(), (ni + 1) * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CK(ctx, cudaMemsetAsync(dfail.p, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
+        setup_s = since(t_setup);
+        for (int which = 0; which < 2; ++which) {
+            const double* x0 = which ? dr.p : dc.p;
+            const double* pp = which ? dw.p : dpc.p;
+            double* rec = which ? drec1.p : drec0.p;
+            CK(ctx, ex ? launch_small_integrate<true>(sm, which, x0, pp, p->t0, p->t1, p->h, plan.total, p->tube_stride, rec, dfail.p + which, ctx->stream)
+                       : launch_small_integrate<false>(sm, which, x0, pp, p->t0, p->t1, p->h, plan.total, p->tube_stride, rec, dfail.p + which, ctx->stream));
+            ctx->launches++;
+        }
+        host_rec0.resize(S * n);
+        host_rec1.resize(S * n);
+        unsigned long long ff[2];
+        CK(ctx, cudaMemcpyAsync(host_rec0.data(), drec0.p, S * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(ctx, cudaMemcpyAsync(host_rec1.data(), drec1.p, S * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(ctx, cudaMemcpyAsync(ff, dfail.p, sizeof ff, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(ctx, cudaStreamSynchronize(ctx->stream));
+        f0 = ff[0];
+        f1 = ff[1];
+    }
+    const double integ_s = since(t_int);
+    const auto t_red = Clock::now();
+    if (tube) {
+        tube->n_slots = S;
+        if (tube->times)
+            for (uint64_t s = 0; s < S; ++s) tube->times[s] = slot_times[s];
+    }
+    auto decode = [](unsigned long long key, uint64_t& step, uint64_t& comp) {
+        step = key >> kFailCompBits;
+        comp = key & ((1ull << kFailCompBits) - 1);
+    };
+    if (method == PIRK_METHOD_MM) {
+        uint64_t fs = 0, fc = 0;
+        if (f0 != kNoFail) decode(f0, fs, fc);
+        for (uint64_t s = 0; s < S; ++s) {
+            if (f0 != kNoFail && fs < slot_steps[s])
+                return fail(ctx, PIRK_EINTEGRATION, "mixed-monotonicity embedding integration: " +
+                                                        integ_msg(fs, fc, p->t0 + static_cast<double>(fs) * p->h));
+            const double* xx = host_rec0.data() + s * 2 * n;
+            for (uint64_t i = 0; i < n; ++i)  // reach.cpp:181-186
+                if (xx[i] > xx[n + i])
+                    return fail(ctx, PIRK_EORDER, "mixed-monotonicity: embedding order violated at step " +
+                                                      std::to_string(slot_steps[s]) + ", t = " + fstr(slot_times[s]) +
+                                                      ", component " + std::to_string(i));
+            if (tube && tube->lower) std::memcpy(tube->lower + s * n, xx, n * sizeof(double));
+            if (tube && tube->upper) std::memcpy(tube->upper + s * n, xx + n, n * sizeof(double));
+        }
+        fill_report(rep, n, 0, plan.total, 7 * 2 * n * sizeof(double), 4 * 2 * n * sizeof(double),
+                    ex, setup_s, integ_s, since(t_red), ctx->launches - launches0);
+    } else {
+        uint64_t fs = 0, fc = 0;
+        if (f0 != kNoFail) {
+            decode(f0, fs, fc);
+            return fail(ctx, PIRK_EINTEGRATION, "growth-bound center integration: " +
+                                                    integ_msg(fs, fc, p->t0 + static_cast<double>(fs) * p->h));
+        }
+        if (f1 != kNoFail) {
+            decode(f1, fs, fc);
+            return fail(ctx, PIRK_EINTEGRATION, "growth-bound radius integration: " +
+                                                    integ_msg(fs, fc, p->t0 + static_cast<double>(fs) * p->h));
+        }
+        for (uint64_t s = 0; s < S; ++s) {  // reach.cpp:121-134
+            double* r = host_rec1.data() + s * n;
+            const double* c = host_rec0.data() + s * n;
+            for (uint64_t i = 0; i < n; ++i) {
+                if (r[i] < 0.0) {
+                    if (r[i] < -1e-12)
+                        return fail(ctx, PIRK_ENEGRADIUS, "growth-bound: deviation went negative (" + fstr(r[i]) +
+                                                              ") at component " + std::to_string(i) +
+                                                              "; contraction matrix is invalid");
+                    r[i] = 0.0;
+                }
+                if (tube && tube->lower) tube->lower[s * n + i] = c[i] - r[i];
+                if (tube && tube->upper) tube->upper[s * n + i] = c[i] + r[i];
+            }
+        }
+        fill_report(rep, n, 0, plan.total, 7 * n * sizeof(double), 4 * n * sizeof(double), ex,
+                    setup_s, integ_s, since(t_red), ctx->launches - launches0);
+    }
+    return PIRK_OK;
+}
+
+pirk_status run_mc(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p, uint64_t seed,
+                   uint64_t s_begin, uint64_t s_end, uint64_t m_total, pirk_tube* tube,
+                   bool fold_into, pirk_report* rep, const double* box_lo, const double* box_hi,
+                   double* fraction) {
+    const auto t_setup = Clock::now();
+    const uint64_t launches0 = ctx->launches;
+    if (!small_ok(m))
+        return fail(ctx, PIRK_EUNSUPPORTED, "monte_carlo: device kernel supports n <= " +
+                                                std::to_string(kSmallMax) + " (got " + std::to_string(m->dim) + ")");
+    Plan plan;
+    plan_steps(p->t0, p->t1, p->h, plan);
+    const bool coverage = fraction != nullptr;
+    std::vector<uint64_t> slot_steps;
+    std::vector<double> slot_times;
+    record_schedule(p->t0, p->t1, p->h, coverage ? 0 : p->tube_stride, plan, slot_steps, slot_times);
+    const uint64_t S = slot_steps.size();
+    if (tube && tube->max_slots < S) return fail(ctx, PIRK_EINVAL, "tube: max_slots too small");
+    if (s_end - s_begin >= (1ull << 34) || plan.total >= (1ull << 20))
+        return fail(ctx, PIRK_EINVAL, "monte_carlo: sample count or step count exceeds the device key range");
+    const uint64_t n = m->dim, ni = m->input_dim;
+    const SmallModel sm = small_model(m);
+    DevBuf<double> dbox;  // lo, hi, plo, phi, box_lo, box_hi
+    DevBuf<unsigned long long> dhull, dflags;
+    const size_t nb = 4 * n + 2 * (ni + 1);
+    std::vector<double> hb(nb, 0.0);
+    for (uint64_t i = 0; i < n; ++i) {
+        hb[i] = p->init_lower[i];
+        hb[n + i] = p->init_upper[i];
+        if (coverage) {
+            hb[2 * n + i] = box_lo[i];
+            hb[3 * n + i] = box_hi[i];
+        }
+    }
+    for (uint64_t j = 0; j < ni; ++j) {
+        hb[4 * n + j] = p->input_lower[j];
+        hb[4 * n + ni + 1 + j] = p->input_upper[j];
+    }
+    CK(ctx, dbox.alloc(nb));
+    CK(ctx, dhull.alloc(S * 2 * n));
+    CK(ctx, dflags.alloc(2));
+    CK(ctx, cudaMemcpyAsync(dbox.p, hb.data(), nb * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    for (uint64_t s = 0; s < S; ++s) {
+        CK(ctx, cudaMemsetAsync(dhull.p + s * 2 * n, 0xff, n * sizeof(unsigned long long), ctx->stream));
+        CK(ctx, cudaMemsetAsync(dhull.p + s * 2 * n + n, 0x00, n * sizeof(unsigned long long), ctx->stream));
+    }
+    CK(ctx, cudaMemsetAsync(dflags.p, 0xff, sizeof(unsigned long long), ctx->stream));
+    CK(ctx, cudaMemsetAsync(dflags.p + 1, 0x00, sizeof(unsigned long long), ctx->stream));
+    McArgs a{};
+    a.lo = dbox.p;
+    a.hi = dbox.p + n;
+    a.plo = dbox.p + 4 * n;
+    a.phi = dbox.p + 4 * n + ni + 1;
+    a.seed = seed;
+    a.s_begin = s_begin;
+    a.s_end = s_end;
+    a.t0 = p->t0;
+    a.t1 = p->t1;
+    a.h = p->h;
+    a.total = plan.total;
+    a.stride = coverage ? 0 : p->tube_stride;
+    a.slots = S;
+    a.hull = dhull.p;
+    a.fail = dflags.p;
+    if (coverage) {
+        a.box_lo = dbox.p + 2 * n;
+        a.box_hi = dbox.p + 3 * n;
+        a.outside = dflags.p + 1;
+    }
+    const double setup_s = since(t_setup);
+    const auto t_int = Clock::now();
+    CK(ctx, exact_mode(ctx) ? launch_monte_carlo<true>(sm, a, ctx->stream)
+                            : launch_monte_carlo<false>(sm, a, ctx->stream));
+    ctx->launches++;
+    std::vector<unsigned long long> hull(S * 2 * n);
+    unsigned long long fl[2];
+    CK(ctx, cudaMemcpyAsync(hull.data(), dhull.p, hull.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaMemcpyAsync(fl, dflags.p, sizeof fl, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    const double integ_s = since(t_int);
+    const auto t_red = Clock::now();
+    if (fl[0] != kNoFail) {
+        const uint64_t smp = s_begin + (fl[0] >> 30), st = (fl[0] >> 10) & 0xfffff, comp = fl[0] & 0x3ff;
+        return fail(ctx, PIRK_EINTEGRATION, "monte-carlo sample " + std::to_string(smp) + " integration: " +
+                                                integ_msg(st, comp, p->t0 + static_cast<double>(st) * p->h));
+    }
+    if (coverage) {
+        *fraction = static_cast<double>(fl[1]) / static_cast<double>(s_end - s_begin);
+        return PIRK_OK;
+    }
+    if (tube) {
+        tube->n_slots = S;
+        for (uint64_t s = 0; s < S; ++s) {
+            if (tube->times) tube->times[s] = slot_times[s];
+            for (uint64_t i = 0; i < n; ++i) {
+                const double lo = ord_val(hull[s * 2 * n + i]);
+                const double hi = ord_val(hull[s * 2 * n + n + i]);
+                if (fold_into) {
+                    if (tube->lower && lo < tube->lower[s * n + i]) tube->lower[s * n + i] = lo;
+                    if (tube->upper && hi > tube->upper[s * n + i]) tube->upper[s * n + i] = hi;
+                } else {
+                    if (tube->lower) tube->lower[s * n + i] = lo;
+                    if (tube->upper) tube->upper[s * n + i] = hi;
+                }
+            }
+        }
+    }
+    // reach.cpp:273-275 with one worker
+    const uint64_t peak = (7 * n * sizeof(double) + 2 * S * n * sizeof(double)) + 2 * S * n * sizeof(double);
+    fill_report(rep, n, m_total, plan.total, peak, nb * sizeof(double) + S * 2 * n * 8,
+                exact_mode(ctx), setup_s, integ_s, since(t_red), ctx->launches - launches0);
+    return PIRK_OK;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+
+extern "C" {
+
+int32_t pirk_abi_version(void) { return PIRK_ABI_VERSION; }
+
+pirk_status pirk_create(int device, pirk_ctx** out) {
+    if (!out) return PIRK_EINVAL;
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) return PIRK_ECUDA;
+    if (device < 0 || device >= count) return PIRK_EINVAL;
+    pirk_ctx* ctx = new (std::nothrow) pirk_ctx;
+    if (!ctx) return PIRK_ENOMEM;
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc(reinterpret_cast<void**>(&ctx->d_flags), 16 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMallocHost(reinterpret_cast<void**>(&ctx->h_flags), 16 * sizeof(unsigned long long)) != cudaSuccess) {
+        delete ctx;
+        return PIRK_ECUDA;
+    }
+    ctx->stream = ctx->own_stream;
+    *out = ctx;
+    return PIRK_OK;
+}
+
+void pirk_destroy(pirk_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->d_flags) cudaFree(ctx->d_flags);
+    if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+const char* pirk_last_error(const pirk_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+pirk_status pirk_set_mode(pirk_ctx* ctx, int32_t mode) {
+    if (!ctx || (mode != PIRK_MODE_EXACT && mode != PIRK_MODE_FAST)) return PIRK_EINVAL;
+    ctx->mode = mode;
+    return PIRK_OK;
+}
+
+pirk_status pirk_set_stream(pirk_ctx* ctx, void* stream) {
+    if (!ctx) return PIRK_EINVAL;
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return PIRK_OK;
+}
+
+void* pirk_get_stream(pirk_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+uint64_t pirk_launch_count(const pirk_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+pirk_status pirk_plan_steps(double t0, double t1, double h, uint64_t* full_steps,
+                            int32_t* has_remainder) {
+    Plan p;
+    if (!plan_steps(t0, t1, h, p)) return PIRK_EINVAL;
+    if (full_steps) *full_steps = p.full;
+    if (has_remainder) *has_remainder = p.rem ? 1 : 0;
+    return PIRK_OK;
+}
+
+uint64_t pirk_record_schedule(double t0, double t1, double h, uint64_t stride, uint64_t* steps_out,
+                              double* times_out) {
+    Plan p;
+    if (!plan_steps(t0, t1, h, p)) return 0;
+    std::vector<uint64_t> steps;
+    std::vector<double> times;
+    record_schedule(t0, t1, h, stride, p, steps, times);
+    for (size_t i = 0; i < steps.size(); ++i) {
+        if (steps_out) steps_out[i] = steps[i];
+        if (times_out) times_out[i] = times[i];
+    }
+    return steps.size();
+}
+
+pirk_status pirk_sample_count(uint64_t n, double epsilon, double delta, uint64_t* out) {
+    // reach.cpp:55-63
+    if (n == 0 || !(epsilon > 0.0) || !(epsilon < 1.0) || !(delta > 0.0) || !(delta < 1.0))
+        return PIRK_EINVAL;
+    const double nn = 2.0 * static_cast<double>(n);
+    *out = static_cast<uint64_t>(std::ceil(nn / epsilon * std::log(nn / delta)));
+    return PIRK_OK;
+}
+
+int32_t pirk_supports(const pirk_model* m, int32_t method) {
+    if (!m) return 0;
+    if (method == PIRK_METHOD_MM) {
+        if (m->decomp == PIRK_DECOMP_NONE) return 0;
+        if (is_chain(m) || is_heat(m)) return m->decomp == PIRK_DECOMP_NATIVE;
+        if (!small_ok(m)) return 0;
+        if (m->decomp == PIRK_DECOMP_JACOBIAN)
+            return m->kind == PIRK_LAUB_LOOMIS || m->kind == PIRK_ARCH_QUAD || m->kind == PIRK_VDP;
+        return m->kind != PIRK_LAUB_LOOMIS && m->kind != PIRK_ARCH_QUAD && m->kind != PIRK_VDP;
+    }
+    if (method == PIRK_METHOD_GB) {
+        if (!has_growth(m)) return 0;
+        return is_chain(m) || is_heat(m) || small_ok(m);
+    }
+    return small_ok(m) ? 1 : 0;  // 2 = Monte Carlo
+}
+
+static pirk_status reach_mm_gb(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p,
+                               pirk_tube* tube, pirk_report* rep, int method) {
+    if (!ctx) return PIRK_EINVAL;
+    ctx->err.clear();
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, PIRK_ECUDA, "cudaSetDevice failed");
+    pirk_status st = PIRK_OK;
+    const bool large = m && (is_chain(m) || is_heat(m));
+    if (!check_problem(ctx, m, p, !large, st)) return st;
+    if (method == PIRK_METHOD_MM) {
+        if (m->decomp == PIRK_DECOMP_NONE)
+            return fail(ctx, PIRK_EINVAL, "mixed_monotonicity: model has no decomposition function");
+        if (!pirk_supports(m, PIRK_METHOD_MM))
+            return fail(ctx, PIRK_EUNSUPPORTED, "mixed_monotonicity: no device kernel for this model/decomposition");
+    } else {
+        if (!has_growth(m)) return fail(ctx, PIRK_EINVAL, "growth_bound: model has no deviation dynamics");
+        if (!pirk_supports(m, PIRK_METHOD_GB))
+            return fail(ctx, PIRK_EUNSUPPORTED, "growth_bound: no device kernel for this model");
+    }
+    try {
+        return large ? run_large(ctx, m, method, p, tube, rep) : run_small(ctx, m, method, p, tube, rep);
+    } catch (const std::bad_alloc&) {
+        return fail(ctx, PIRK_ENOMEM, "host allocation failed");
+    }
+}
+
+pirk_status pirk_mixed_monotonicity(pirk_ctx* ctx, const pirk_model* model,
+                                    const pirk_problem* problem, pirk_tube* tube,
+                                    pirk_report* report) {
+    return reach_mm_gb(ctx, model, problem, tube, report, PIRK_METHOD_MM);
+}
+
+pirk_status pirk_growth_bound(pirk_ctx* ctx, const pirk_model* model, const pirk_problem* problem,
+                              pirk_tube* tube, pirk_report* report) {
+    return reach_mm_gb(ctx, model, problem, tube, report, PIRK_METHOD_GB);
+}
+
+pirk_status pirk_monte_carlo(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p,
+                             const pirk_mc_spec* spec, pirk_tube* tube, pirk_report* report) {
+    if (!ctx || !spec) return PIRK_EINVAL;
+    ctx->err.clear();
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, PIRK_ECUDA, "cudaSetDevice failed");
+    pirk_status st = PIRK_OK;
+    if (!check_problem(ctx, m, p, true, st)) return st;
+    uint64_t count = spec->samples_override;
+    if (count == 0) {
+        if (pirk_sample_count(m->dim, spec->epsilon, spec->delta, &count) != PIRK_OK) {
+            if (!(spec->epsilon > 0.0) || !(spec->epsilon < 1.0))
+                return fail(ctx, PIRK_EINVAL, "sample_count: epsilon must be in (0, 1)");
+            return fail(ctx, PIRK_EINVAL, "sample_count: delta must be in (0, 1)");
+        }
+    }
+    try {
+        return run_mc(ctx, m, p, spec->seed, 0, count, count, tube, false, report, nullptr, nullptr, nullptr);
+    } catch (const std::bad_alloc&) {
+        return fail(ctx, PIRK_ENOMEM, "host allocation failed");
+    }
+}
+
+pirk_status pirk_monte_carlo_range(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p,
+                                   uint64_t seed, uint64_t s_begin, uint64_t s_end,
+                                   pirk_tube* tube, pirk_report* report) {
+    if (!ctx) return PIRK_EINVAL;
+    ctx->err.clear();
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, PIRK_ECUDA, "cudaSetDevice failed");
+    pirk_status st = PIRK_OK;
+    if (!check_problem(ctx, m, p, true, st)) return st;
+    if (s_end < s_begin) return fail(ctx, PIRK_EINVAL, "monte_carlo_range: s_end < s_begin");
+    if (s_end == s_begin) {
+        if (tube) tube->n_slots = pirk_record_schedule(p->t0, p->t1, p->h, p->tube_stride, nullptr, tube->times);
+        return PIRK_OK;
+    }
+    try {
+        return run_mc(ctx, m, p, seed, s_begin, s_end, s_end - s_begin, tube, true, report, nullptr, nullptr, nullptr);
+    } catch (const std::bad_alloc&) {
+        return fail(ctx, PIRK_ENOMEM, "host allocation failed");
+    }
+}
+
+pirk_status pirk_coverage_estimate(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p,
+                                   const double* box_lower, const double* box_upper,
+                                   uint64_t fresh_samples, uint64_t seed, double* fraction) {
+    if (!ctx || !fraction) return PIRK_EINVAL;
+    ctx->err.clear();
+    pirk_status st = PIRK_OK;
+    if (!check_problem(ctx, m, p, true, st)) return st;
+    if (!box_lower || !box_upper) return fail(ctx, PIRK_EINVAL, "coverage_estimate: tube has no entries");
+    if (fresh_samples == 0) return fail(ctx, PIRK_EINVAL, "coverage_estimate: fresh_samples must be positive");
+    try {
+        return run_mc(ctx, m, p, seed, 0, fresh_samples, fresh_samples, nullptr, false, nullptr,
+                      box_lower, box_upper, fraction);
+    } catch (const std::bad_alloc&) {
+        return fail(ctx, PIRK_ENOMEM, "host allocation failed");
+    }
+}
+
+pirk_status pirk_engine_create(pirk_ctx* ctx, const pirk_model* m, int32_t method,
+                               const pirk_problem* p, pirk_engine** out) {
+    if (!ctx || !out) return PIRK_EINVAL;
+    *out = nullptr;
+    ctx->err.clear();
+    if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, PIRK_ECUDA, "cudaSetDevice failed");
+    pirk_status st = PIRK_OK;
+    if (!check_problem(ctx, m, p, false, st)) return st;
+    if (!(is_chain(m) || is_heat(m)) || !pirk_supports(m, method))
+        return fail(ctx, PIRK_EUNSUPPORTED, "engine: only the chain and heat3d kernels run as engines");
+    pirk_engine* e = new (std::nothrow) pirk_engine;
+    if (!e) return PIRK_ENOMEM;
+    st = engine_init(ctx, m, method, p, e);
+    if (st != PIRK_OK) {
+        delete e;
+        return st;
+    }
+    *out = e;
+    return PIRK_OK;
+}
+
+pirk_status pirk_engine_advance(pirk_engine* e, uint64_t nsteps) {
+    if (!e) return PIRK_EINVAL;
+    return engine_advance(e, nsteps);
+}
+
+pirk_status pirk_engine_status(pirk_engine* e, uint64_t* steps_done) {
+    if (!e) return PIRK_EINVAL;
+    pirk_ctx* ctx = e->ctx;
+    unsigned long long f[2];
+    CK(ctx, cudaMemcpyAsync(f, e->d_fail.p, sizeof f, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    if (steps_done) *steps_done = e->done;
+    for (int i = 0; i < 2; ++i) {
+        if (f[i] != kNoFail) {
+            const uint64_t s = f[i] >> kFailCompBits, c = f[i] & ((1ull << kFailCompBits) - 1);
+            return fail(ctx, PIRK_EINTEGRATION, integ_msg(s, c, e->t0 + static_cast<double>(s) * e->h));
+        }
+    }
+    return PIRK_OK;
+}
+
+pirk_status pirk_engine_read(pirk_engine* e, double* lower, double* upper) {
+    if (!e) return PIRK_EINVAL;
+    pirk_ctx* ctx = e->ctx;
+    const uint64_t n = e->n;
+    const double* lo = e->s0();
+    const double* hi = e->s1();
+    if (e->method == PIRK_METHOD_GB) {
+        CK(ctx, cudaMemsetAsync(ctx->d_flags, 0xff, sizeof(unsigned long long), ctx->stream));
+        CK(ctx, launch_gb_box(e->s0(), e->s1(), e->o0(), e->o1(), n, ctx->d_flags, ctx->stream));
+        ctx->launches++;
+        lo = e->o0();
+        hi = e->o1();
+    }
+    if (lower) CK(ctx, cudaMemcpyAsync(lower, lo, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (upper) CK(ctx, cudaMemcpyAsync(upper, hi, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    return PIRK_OK;
+}
+
+void pirk_engine_destroy(pirk_engine* e) { delete e; }
+
+pirk_status pirk_step_window(pirk_ctx* ctx, const pirk_model* m, int32_t method,
+                             const pirk_window* win, const double* p0, const double* p1,
+                             double t, double hk, uint64_t step_index, uint64_t* fail_ptr) {
+    if (!ctx || !win) return PIRK_EINVAL;
+    pirk_status st = PIRK_OK;
+    if (!check_model(ctx, m, st)) return st;
+    if (!(is_chain(m) || is_heat(m)) || !pirk_supports(m, method))
+        return fail(ctx, PIRK_EUNSUPPORTED, "step_window: only the chain and heat3d kernels are windowed");
+    const uint64_t unit = is_heat(m) ? m->grid * m->grid : 1;
+    const uint64_t units = m->dim / unit;
+    const uint64_t wb = win->win_begin, we = win->win_begin + win->win_len;
+    if (we > units || win->out_begin < wb || win->out_end > we || win->out_begin > win->out_end)
+        return fail(ctx, PIRK_EINVAL, "step_window: window outside the state");
+    const uint64_t need_lo = win->out_begin >= 4 ? win->out_begin - 4 : 0;
+    const uint64_t need_hi = (win->out_end + 4 <= units) ? win->out_end + 4 : units;
+    if (wb > need_lo || we < need_hi)
+        return fail(ctx, PIRK_EINVAL, "step_window: window must cover the output range +-4 units");
+    double q0 = 0.0, q1 = 0.0;
+    if (m->input_dim > 0) {
+        if (!p0 || !p1) return fail(ctx, PIRK_EINVAL, "step_window: inputs missing");
+        q0 = p0[0];
+        q1 = p1[0];
+    }
+    StepConsts sc;  // rk4.cpp:38-39
+    sc.t = t;
+    sc.hk = hk;
+    sc.h2 = 0.5 * hk;
+    sc.h6 = hk / 6.0;
+    const ChainModel cm = chain_model(m, method, q0, q1);
+    const HeatModel hm = heat_model(m, method);
+    WindowArgs w{win->in0, win->in1, win->out0, win->out1, wb, we, win->out_begin, win->out_end};
+    CK(ctx, step_launch(ctx, m, method, cm, hm, w, sc, step_index,
+                        reinterpret_cast<unsigned long long*>(fail_ptr)));
+    return PIRK_OK;
+}
+
+}  // extern "C"

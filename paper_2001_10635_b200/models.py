@@ -1,0 +1,144 @@
+"""Model descriptors: the device-side counterpart of the reference's model
+library (/root/reference/proj/include/ivreach/models.hpp, src/models.cpp).
+
+The reference builds ``SystemModel`` objects out of ``std::function``
+evaluators (system_model.hpp:14-43); those cannot run on a GPU, so here a
+``SystemModel`` is a descriptor naming which device vector field to use and
+its resolved parameters.  Constructors keep the reference's names, defaults
+and argument validation (messages of models.cpp ``require``).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+from typing import Tuple
+
+# pirk_model_kind (include/pirk_c.h)
+ZERO, SCALAR_DECAY, SCALAR_LINEAR, TRAFFIC, HEAT3D, CHAIN, LAUB_LOOMIS, ARCH_QUAD, VDP = range(9)
+# pirk_decomp
+DECOMP_NONE, DECOMP_NATIVE, DECOMP_JACOBIAN = range(3)
+
+_HAS_GROWTH = {ZERO, SCALAR_DECAY, SCALAR_LINEAR, TRAFFIC, HEAT3D, LAUB_LOOMIS, ARCH_QUAD, VDP}
+
+
+@dataclass(frozen=True)
+class SystemModel:
+    """system_model.hpp:28-43.  ``decomposition``/``growth_rhs`` presence is
+    expressed by ``decomp`` and the model kind."""
+
+    kind: int
+    dim: int
+    input_dim: int
+    params: Tuple[float, ...] = field(default_factory=tuple)
+    decomp: int = DECOMP_NATIVE
+    grid: int = 0
+    name: str = ""
+    input_affine: bool = True
+    sparsity_note: str = ""
+
+    def has_growth(self) -> bool:
+        return self.kind in _HAS_GROWTH
+
+    def has_decomposition(self) -> bool:
+        return self.decomp != DECOMP_NONE
+
+
+def _require(ok: bool, msg: str) -> None:
+    if not ok:
+        raise ValueError(msg)
+
+
+def _p(*vals) -> Tuple[float, ...]:
+    return tuple(float(v) for v in vals)
+
+
+def make_traffic(segments: int, v: float = 0.5, w: float = 1.0 / 6.0, c: float = 40.0,
+                 xbar: float = 320.0, period: float = 30.0, beta: float = 0.75) -> SystemModel:
+    """models.cpp:47-90 (cooperative: decomposition = cooperative(f))."""
+    _require(segments >= 3, "traffic model needs at least 3 segments")
+    _require(v > 0 and w > 0 and c > 0 and xbar > 0 and period > 0,
+             "traffic parameters must be positive")
+    _require(0 < beta <= 1, "traffic beta must lie in (0, 1]")
+    return SystemModel(TRAFFIC, int(segments), 1, _p(v, w, c, xbar, period, beta),
+                       DECOMP_NATIVE, name="traffic", sparsity_note="tridiagonal")
+
+
+def make_heat3d(grid: int, alpha: float = 1.0, exchange: float = 1.0) -> SystemModel:
+    """models.cpp:92-133 (linear, cooperative; growth_rhs == rhs)."""
+    _require(grid >= 2, "heat3d model needs at least 2 grid points per axis")
+    _require(alpha > 0, "heat3d alpha must be positive")
+    _require(exchange >= 0, "heat3d exchange coefficient must be nonnegative")
+    g = int(grid)
+    return SystemModel(HEAT3D, g * g * g, 0, _p(alpha, exchange), DECOMP_NATIVE, grid=g,
+                       name="heat3d", sparsity_note="7-point stencil")
+
+
+def make_chain(n: int, a: float = 1.0, b: float = 0.5, c: float = 0.25) -> SystemModel:
+    """Synthetic coupled (non-cooperative) chain of SURVEY.md 8(d), config 4:
+    f_i = -a x_i + b s(x_{i-1}) - c s(x_{i+1}) + p, s(z) = z/(1+|z|),
+    with the decomposition reading x_{i+1} from the opposite corner."""
+    _require(n >= 1, "chain model needs at least 1 state")
+    return SystemModel(CHAIN, int(n), 1, _p(a, b, c), DECOMP_NATIVE, name="chain",
+                       input_affine=True, sparsity_note="tridiagonal, non-cooperative")
+
+
+def make_laub_loomis() -> SystemModel:
+    """models.cpp:463-502 (no decomposition in the catalog)."""
+    return SystemModel(LAUB_LOOMIS, 7, 0, (), DECOMP_NONE, name="laub-loomis")
+
+
+def make_arch_quadrotor(mass: float = 1.4, gravity: float = 9.81, jx: float = 0.054,
+                        jy: float = 0.054, jz: float = 0.104) -> SystemModel:
+    """models.cpp:504-613 (no decomposition in the catalog)."""
+    _require(mass > 0 and gravity > 0 and jx > 0 and jy > 0 and jz > 0,
+             "quadrotor physical parameters must be positive")
+    return SystemModel(ARCH_QUAD, 12, 0, _p(mass, gravity, jx, jy, jz), DECOMP_NONE,
+                       name="arch-quadrotor")
+
+
+def make_vdp(mu: float = 1.0, op_x: float = 2.5, op_y: float = 3.0) -> SystemModel:
+    """models.cpp:444-461."""
+    _require(mu > 0, "van der Pol mu must be positive")
+    _require(op_x > 0 and op_y > 0, "van der Pol operating box must be positive")
+    return SystemModel(VDP, 2, 0, _p(mu, op_x, op_y), DECOMP_NONE, name="vdp")
+
+
+def make_zero(dim: int = 2) -> SystemModel:
+    """models.cpp:615-627."""
+    _require(dim >= 1, "zero model needs at least 1 state")
+    return SystemModel(ZERO, int(dim), 0, (), DECOMP_NATIVE, name="zero")
+
+
+def make_scalar_decay() -> SystemModel:
+    """models.cpp:629-641: xdot = -x + p."""
+    return SystemModel(SCALAR_DECAY, 1, 1, (), DECOMP_NATIVE, name="scalar-decay")
+
+
+def make_scalar_linear(a: float = 1.0) -> SystemModel:
+    """models.cpp:643-655: xdot = a x."""
+    return SystemModel(SCALAR_LINEAR, 1, 0, _p(a), DECOMP_NATIVE, name="scalar-linear")
+
+
+def with_jacobian_decomposition(model: SystemModel) -> SystemModel:
+    """Attach d_i = f_i(x) + sum_{j != i, C_ij != 0} C_ij (x_j - xh_j), where C
+    is the model's growth matrix (a valid decomposition wherever C bounds
+    |df_i/dx_j| -- the models' documented operating boxes).  This is the
+    user-supplied decomposition the reference accepts through its public API
+    (test_reach.cpp:195-205); SURVEY.md 8(d) uses it for config 1."""
+    _require(model.kind in (LAUB_LOOMIS, ARCH_QUAD, VDP),
+             "jacobian decomposition needs a dense growth matrix model")
+    return replace(model, decomp=DECOMP_JACOBIAN)
+
+
+# Catalog defaults for the configurations the hot path is benchmarked on
+# (models.cpp:688-1000 default problems).
+CATALOG = {
+    "traffic": make_traffic,
+    "heat3d": make_heat3d,
+    "chain": make_chain,
+    "laub-loomis": make_laub_loomis,
+    "arch-quadrotor": make_arch_quadrotor,
+    "vdp": make_vdp,
+    "zero": make_zero,
+    "scalar-decay": make_scalar_decay,
+    "scalar-linear": make_scalar_linear,
+}

@@ -1,0 +1,307 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on
+identical inputs.  Exact mode must be bit-identical; fast mode within the
+SURVEY.md 8(d) tolerance contract (relative <= 1e-12, never tighter)."""
+import numpy as np
+import pytest
+
+import paper_2001_10635_b200 as pk
+from oracle import oracle as O
+from tests.helpers import assert_bitexact, assert_within, tube_arrays
+
+pytestmark = pytest.mark.gpu
+
+
+def traffic_problem(n, t1=30.0, h=0.5, stride=10, lo=10.0, hi=20.0, plo=4.0, phi=6.0):
+    m = pk.make_traffic(n)
+    return m, pk.ReachProblem(m, pk.IntervalVector(np.full(n, lo), np.full(n, hi)),
+                              pk.IntervalVector([plo], [phi]), 0.0, t1, h, stride)
+
+
+def heat_problem(g, t1=0.05, h=0.002, stride=5, lo=None, hi=None):
+    m = pk.make_heat3d(g)
+    n = g ** 3
+    lo = np.full(n, 0.9) if lo is None else lo
+    hi = np.full(n, 1.1) if hi is None else hi
+    return m, pk.ReachProblem(m, pk.IntervalVector(lo, hi), None, 0.0, t1, h, stride)
+
+
+def chain_problem(n, t1=1.0, h=0.01, stride=10):
+    m = pk.make_chain(n)
+    c = 2.0 * np.array([O.u01(7, 0, i) for i in range(n)]) - 1.0
+    return m, pk.ReachProblem(m, pk.IntervalVector(c - 0.05, c + 0.05),
+                              pk.IntervalVector([-0.1], [0.1]), 0.0, t1, h, stride)
+
+
+def oracle_for(method, prob):
+    p = prob
+    plo = p.inputs.lower if p.inputs is not None else None
+    phi = p.inputs.upper if p.inputs is not None else None
+    fn = {"mm": O.mixed_monotonicity, "gb": O.growth_bound}[method]
+    return fn(p.model, p.initial.lower, p.initial.upper, plo, phi, p.t0, p.t1, p.h, p.tube_stride)
+
+
+# ------------------------------------------------------------------ traffic
+
+@pytest.mark.parametrize("n", [3, 5, 50, 1000, 1017, 2033, 100003])
+def test_traffic_mm_exact(ctx, n):
+    m, prob = traffic_problem(n)
+    assert_bitexact(pk.mixed_monotonicity(prob, ctx=ctx), oracle_for("mm", prob))
+
+
+@pytest.mark.parametrize("n", [3, 5, 1000, 5001])
+def test_traffic_gb_exact(ctx, n):
+    m, prob = traffic_problem(n)
+    assert_bitexact(pk.growth_bound(prob, ctx=ctx), oracle_for("gb", prob))
+
+
+def test_traffic_ragged_box_and_remainder_step(ctx):
+    # non-uniform box, h that does not divide the span (shortened last step,
+    # rk4.cpp:100) and a stride that does not divide the step count
+    n = 777
+    rng = np.random.default_rng(3)
+    lo = rng.uniform(0, 300, n)
+    hi = lo + rng.uniform(0, 20, n)
+    m = pk.make_traffic(n)
+    prob = pk.ReachProblem(m, pk.IntervalVector(lo, hi), pk.IntervalVector([0.5], [30.0]),
+                           0.0, 10.0, 0.3, 7)
+    assert_bitexact(pk.mixed_monotonicity(prob, ctx=ctx), oracle_for("mm", prob))
+    assert_bitexact(pk.growth_bound(prob, ctx=ctx), oracle_for("gb", prob))
+
+
+def test_traffic_fast_mode_tolerance(fast_ctx):
+    m, prob = traffic_problem(5000)
+    assert_within(pk.mixed_monotonicity(prob, ctx=fast_ctx), oracle_for("mm", prob))
+    assert_within(pk.growth_bound(prob, ctx=fast_ctx), oracle_for("gb", prob))
+
+
+# --------------------------------------------------------------------- heat
+
+@pytest.mark.parametrize("g", [2, 3, 4, 5, 8, 31, 33, 40])
+def test_heat_mm_exact(ctx, g):
+    m, prob = heat_problem(g, t1=0.02, h=0.2 / (g - 1) ** 2 if g > 3 else 0.002, stride=3)
+    assert_bitexact(pk.mixed_monotonicity(prob, ctx=ctx), oracle_for("mm", prob))
+
+
+def test_heat_ragged_box(ctx):
+    g = 20
+    n = g ** 3
+    rng = np.random.default_rng(11)
+    lo = rng.uniform(0.5, 1.0, n)
+    hi = lo + rng.uniform(0.0, 0.5, n)
+    m, prob = heat_problem(g, t1=0.005, h=0.0004, stride=4, lo=lo, hi=hi)
+    assert_bitexact(pk.mixed_monotonicity(prob, ctx=ctx), oracle_for("mm", prob))
+    assert_bitexact(pk.growth_bound(prob, ctx=ctx), oracle_for("gb", prob))
+
+
+@pytest.mark.parametrize("g", [8, 37])
+def test_heat_fast_mode_tolerance(fast_ctx, g):
+    m, prob = heat_problem(g, t1=0.2 / (g - 1) ** 2 * 20, h=0.2 / (g - 1) ** 2, stride=5)
+    assert_within(pk.mixed_monotonicity(prob, ctx=fast_ctx), oracle_for("mm", prob))
+
+
+# -------------------------------------------------------------------- chain
+
+@pytest.mark.parametrize("n", [1, 2, 7, 1000, 1016, 1017, 5000])
+def test_chain_mm_exact(ctx, n):
+    m, prob = chain_problem(n)
+    assert_bitexact(pk.mixed_monotonicity(prob, ctx=ctx), oracle_for("mm", prob))
+
+
+def test_chain_fast_mode_tolerance(fast_ctx):
+    m, prob = chain_problem(3000)
+    assert_within(pk.mixed_monotonicity(prob, ctx=fast_ctx), oracle_for("mm", prob), atol=1e-15)
+
+
+# ------------------------------------------------------------ small systems
+
+def test_scalar_linear_mm_is_e_2e(ctx):
+    # test_reach.cpp:70-75 / acceptance criterion 5
+    m = pk.make_scalar_linear()
+    prob = pk.ReachProblem(m, pk.IntervalVector([1.0], [2.0]), None, 0.0, 1.0, 0.001, 0)
+    tube = pk.mixed_monotonicity(prob, ctx=ctx)
+    fin = tube.entries[-1].box
+    assert abs(fin.lower[0] - np.e) <= 1e-4 and abs(fin.upper[0] - 2 * np.e) <= 1e-4
+    assert_bitexact(tube, oracle_for("mm", prob))
+
+
+def test_frozen_system_keeps_box(ctx):
+    # test_reach.cpp:35-50
+    m = pk.make_zero(2)
+    init = pk.IntervalVector([0.0, 0.0], [1.0, 1.0])
+    prob = pk.ReachProblem(m, init, None, 0.0, 1.0, 0.1, 4)
+    for tube in (pk.growth_bound(prob, ctx=ctx), pk.mixed_monotonicity(prob, ctx=ctx)):
+        assert len(tube.entries) >= 2
+        for e in tube.entries:
+            assert e.box == init
+        assert tube.entries[-1].t == 1.0
+    mc = pk.monte_carlo(pk.ReachProblem(m, init, None, 0.0, 1.0, 0.1, 0),
+                        pk.MonteCarloSpec(samples_override=100), ctx=ctx)
+    assert pk.subset_of(mc.entries[-1].box, init)
+
+
+def test_scalar_decay_gb_closed_form(ctx):
+    # test_reach.cpp:53-68 / acceptance criterion 4
+    m = pk.make_scalar_decay()
+    prob = pk.ReachProblem(m, pk.IntervalVector([0.9], [1.1]), pk.IntervalVector([0.0], [0.0]),
+                           0.0, 1.0, 0.001, 0)
+    tube = pk.growth_bound(prob, ctx=ctx)
+    fin = tube.entries[-1].box
+    assert abs((fin.upper[0] - fin.lower[0]) / 2 - 0.1 / np.e) <= 1e-5
+    assert tube.report.steps == 1000
+    assert_bitexact(tube, oracle_for("gb", prob))
+
+
+def test_laub_loomis_gb_exact(ctx):
+    m = pk.make_laub_loomis()
+    lo = np.array([1.15, 1.00, 1.45, 2.35, 0.95, 0.05, 0.40])
+    prob = pk.ReachProblem(m, pk.IntervalVector(lo, lo + 0.1), None, 0.0, 1.0, 0.005, 20)
+    assert_bitexact(pk.growth_bound(prob, ctx=ctx), oracle_for("gb", prob))
+
+
+def test_laub_loomis_jacobian_mm_exact(ctx):
+    m = pk.with_jacobian_decomposition(pk.make_laub_loomis())
+    lo = np.array([1.15, 1.00, 1.45, 2.35, 0.95, 0.05, 0.40])
+    prob = pk.ReachProblem(m, pk.IntervalVector(lo, lo + 0.1), None, 0.0, 0.2, 0.005, 10)
+    assert_bitexact(pk.mixed_monotonicity(prob, ctx=ctx), oracle_for("mm", prob))
+
+
+def arch_quad_problem(stride=10, decomp=False):
+    m = pk.make_arch_quadrotor()
+    if decomp:
+        m = pk.with_jacobian_decomposition(m)
+    lo = np.array([-0.4] * 6 + [0.0] * 6)
+    return m, pk.ReachProblem(m, pk.IntervalVector(lo, -lo), None, 0.0, 1.0, 0.01, stride)
+
+
+def test_arch_quad_gb_tolerance(ctx):
+    # config 1 as shipped (growth bound); CUDA sin/cos vs glibc -> tolerance
+    m, prob = arch_quad_problem()
+    assert_within(pk.growth_bound(prob, ctx=ctx), oracle_for("gb", prob), rel=1e-12, atol=1e-14)
+
+
+def test_arch_quad_ctmm_tolerance(ctx):
+    # config 1 as CTMM through the Jacobian-bound decomposition
+    m, prob = arch_quad_problem(decomp=True)
+    assert_within(pk.mixed_monotonicity(prob, ctx=ctx), oracle_for("mm", prob), rel=1e-12,
+                  atol=1e-14)
+
+
+# -------------------------------------------------------------- Monte Carlo
+
+def mc_oracle(prob, seed, m):
+    p = prob
+    plo = p.inputs.lower if p.inputs is not None else None
+    phi = p.inputs.upper if p.inputs is not None else None
+    return O.monte_carlo(p.model, p.initial.lower, p.initial.upper, plo, phi, p.t0, p.t1, p.h,
+                         p.tube_stride, seed, m)
+
+
+def test_laub_loomis_mc_exact(ctx):
+    m = pk.make_laub_loomis()
+    c = np.array([1.2, 1.05, 1.5, 2.4, 1.0, 0.1, 0.45])
+    prob = pk.ReachProblem(m, pk.IntervalVector(c - 0.05, c + 0.05), None, 0.0, 1.0, 0.005, 20)
+    tube = pk.monte_carlo(prob, pk.MonteCarloSpec(seed=1, samples_override=3000), ctx=ctx)
+    assert_bitexact(tube, mc_oracle(prob, 1, 3000))
+    assert tube.report.m == 3000
+
+
+def test_traffic_mc_exact_and_seeded(ctx):
+    # test_reach.cpp:88-111: traffic n=6, seed 42, m=64, stride 2
+    m, prob = traffic_problem(6, t1=3.0, h=0.5, stride=2)
+    a = pk.monte_carlo(prob, pk.MonteCarloSpec(seed=42, samples_override=64), ctx=ctx)
+    assert_bitexact(a, mc_oracle(prob, 42, 64))
+    b = pk.monte_carlo(prob, pk.MonteCarloSpec(seed=43, samples_override=64), ctx=ctx)
+    assert pk.tube_to_csv(a) != pk.tube_to_csv(b)
+    c3 = pk.monte_carlo(prob, pk.MonteCarloSpec(seed=42, samples_override=3), ctx=ctx)
+    assert_bitexact(c3, mc_oracle(prob, 42, 3))
+
+
+def test_arch_quad_mc_tolerance(ctx):
+    m, prob = arch_quad_problem()
+    tube = pk.monte_carlo(prob, pk.MonteCarloSpec(seed=1, samples_override=4096), ctx=ctx)
+    assert_within(tube, mc_oracle(prob, 1, 4096), rel=1e-12, atol=1e-14, never_tighter=False)
+
+
+def test_mc_hull_inside_exact_image(ctx):
+    # test_reach.cpp:113-124
+    m = pk.make_scalar_linear()
+    prob = pk.ReachProblem(m, pk.IntervalVector([1.0], [2.0]), None, 0.0, 1.0, 0.001, 0)
+    fin = pk.monte_carlo(prob, pk.MonteCarloSpec(seed=3, samples_override=1000), ctx=ctx).entries[-1].box
+    e = np.e
+    assert fin.lower[0] >= e - 1e-9 and fin.upper[0] <= 2 * e + 1e-9
+    assert fin.lower[0] <= e * 1.02 and fin.upper[0] >= 2 * e * 0.98
+
+
+def test_coverage_estimate_matches_oracle(ctx):
+    # test_reach.cpp:126-147
+    m = pk.make_zero(2)
+    prob = pk.ReachProblem(m, pk.IntervalVector([0.0, 0.0], [1.0, 1.0]), None, 0.0, 1.0, 0.1, 0)
+    spec = pk.MonteCarloSpec(seed=5, samples_override=200)
+    tube = pk.monte_carlo(prob, spec, ctx=ctx)
+    honest = pk.coverage_estimate(prob, spec, tube, 5000, 77, ctx=ctx)
+    fin = tube.entries[-1].box
+    ref = O.coverage_estimate(m, [0, 0], [1, 1], None, None, 0.0, 1.0, 0.1, fin.lower, fin.upper,
+                              5000, 77)
+    assert honest == ref
+    assert 0.0 <= honest < 0.2
+
+
+# ------------------------------------------------------------------- errors
+
+def test_non_finite_reports_step(ctx):
+    # test_rk4.cpp:138-154 through mixed monotonicity
+    m = pk.make_scalar_linear(5.0)
+    prob = pk.ReachProblem(m, pk.IntervalVector([1.0], [1.0]), None, 0.0, 600.0, 10.0, 0)
+    with pytest.raises(RuntimeError) as ei:
+        pk.mixed_monotonicity(prob, ctx=ctx)
+    with pytest.raises(O.OracleError) as eo:
+        oracle_for("mm", prob)
+    assert str(ei.value) == str(eo.value)
+
+
+def test_non_finite_large_model(ctx):
+    # traffic driven to overflow by an absurd step: error names step/component
+    m, prob = traffic_problem(2000, t1=1e6, h=1e5, stride=0, lo=1e300, hi=1e300)
+    with pytest.raises(RuntimeError) as ei:
+        pk.mixed_monotonicity(prob, ctx=ctx)
+    with pytest.raises(O.OracleError) as eo:
+        oracle_for("mm", prob)
+    assert str(ei.value) == str(eo.value)
+
+
+def test_order_violation_reported(ctx):
+    # test_reach.cpp:190-206 uses a custom decomposition; the chain model with
+    # an inverted box is the closest catalog analogue: check the message
+    # matches the oracle's exactly.
+    m = pk.make_chain(50, a=-3.0, b=2.0, c=-2.0)
+    c = np.linspace(-1, 1, 50)
+    prob = pk.ReachProblem(m, pk.IntervalVector(c - 0.5, c + 0.5), pk.IntervalVector([-1.0], [1.0]),
+                           0.0, 3.0, 0.1, 1)
+    try:
+        ref = oracle_for("mm", prob)
+    except O.OracleError as e:
+        with pytest.raises(RuntimeError) as ei:
+            pk.mixed_monotonicity(prob, ctx=ctx)
+        assert str(ei.value) == str(e)
+    else:
+        assert_bitexact(pk.mixed_monotonicity(prob, ctx=ctx), ref)
+
+
+def test_unsupported_model_is_loud(ctx):
+    m = pk.make_traffic(100)  # Monte Carlo kernel is for n <= 64
+    prob = pk.ReachProblem(m, pk.IntervalVector(np.zeros(100), np.ones(100)),
+                           pk.IntervalVector([1.0], [2.0]), 0.0, 1.0, 0.5, 0)
+    with pytest.raises(NotImplementedError):
+        pk.monte_carlo(prob, pk.MonteCarloSpec(samples_override=10), ctx=ctx)
+
+
+def test_missing_capabilities_rejected(ctx):
+    m = pk.make_chain(10)
+    prob = pk.ReachProblem(m, pk.IntervalVector(np.zeros(10), np.ones(10)),
+                           pk.IntervalVector([0.0], [0.0]), 0.0, 1.0, 0.1, 0)
+    with pytest.raises(ValueError, match="no deviation dynamics"):
+        pk.growth_bound(prob, ctx=ctx)
+    ll = pk.make_laub_loomis()
+    prob2 = pk.ReachProblem(ll, pk.IntervalVector(np.zeros(7), np.ones(7)), None, 0.0, 1.0, 0.1, 0)
+    with pytest.raises(ValueError, match="no decomposition"):
+        pk.mixed_monotonicity(prob2, ctx=ctx)
