@@ -175,7 +175,7 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
                     const double kv = heat_point<Exact>(
                         s, s_c[si - 1], s_c[si + 1], s_c[si - Ws], s_c[si + Ws], s_m[si], s_p[si],
                         ix > 0, ix + 1 < g, iy > 0, iy + 1 < g, hz_m, hz_p, hp.robin, hp.kk);
-                    const double xv = xc[(y + off) * kHeatW0 + (x + off)];
+                    const double xv = xc[(y + L) * kHeatW0 + (x + L)];  // level-L (x,y) is level-0 (x+L, y+L)
                     const int ax = x - off, ay = y - off;  // accumulator coordinates
                     const bool own = ax >= 0 && ax < kHeatT && ay >= 0 && ay < kHeatT;
                     const int ai = ay * kHeatT + ax;
