@@ -5,84 +5,262 @@
 // independently and each is the plain stencil) and on the growth-bound pair
 // (growth_rhs == rhs for heat3d, models.cpp:130).
 //
-// Design (2.5-D z-streaming): a CTA owns a 32x32 x-y tile of one field and
-// streams z.  Iteration j loads plane j (x-y halo 4, cp.async, one plane of
-// prefetch), then computes
-//     stage 1 (k0, u1) at plane j-1 on the tile + halo 3,
-//     stage 2 (k1, u2) at plane j-2 on the tile + halo 2,
-//     stage 3 (k2, u3) at plane j-3 on the tile + halo 1,
-//     stage 4 (k3, x') at plane j-4 on the tile,
-// keeping rings of planes for x (6), u1/u2/u3 (3 each) and the RK
-// accumulator (4) in shared memory.  HBM sees each x once and each x' once:
-// 16 B per state-update.
+// Design (2.5-D z-streaming).  A CTA of 512 threads owns a 32x32 x-y tile of
+// one field and streams z.  Iteration j
+//     - issues the global loads of x-plane j+1 (tile + halo 4) into registers,
+//     - stage 1 (k0, u1) at plane j-1 on the tile + halo 3,
+//     - stage 2 (k1, u2) at plane j-2 on the tile + halo 2,
+//     - stage 3 (k2, u3) at plane j-3 on the tile + halo 1,
+//     - stage 4 (k3, x') at plane j-4 on the tile, stored to HBM,
+//     - writes plane j+1 into the shared-memory x ring.
+// Shared memory holds rings of planes (x: 5, u1/u2/u3: 3 each), all with the
+// same 40x40 pitch so every buffer uses the same neighbour offsets.  Each
+// thread owns two tile points (rows t/32 and t/32+16) whose RK accumulator
+// and x values live in registers across the four lagged stages, plus at most
+// one point of each level's halo ring; all shared-memory offsets are computed
+// once per CTA.  HBM sees each x once and each x' once: 16 B/state-update.
+//
+// Boundaries.  Interior tiles (the halo-4 footprint inside the grid in x and
+// y) run without per-point checks.  The insulated z faces use the centre
+// plane as the missing neighbour: the term (s - s) = +0.0 leaves the sum
+// unchanged exactly as skipping it does (the running sum is never -0.0: it
+// starts at +0.0 and round-to-nearest sums of nonzero terms are never -0).
+// Edge tiles evaluate models.cpp:113-126 with per-point face flags.
 //
 // Exact mode evaluates models.cpp:113-126 literally (acc = 0.0; acc += ...
-// in the order x-, x+, y-, y+, z-, z+; the Robin ghost at ix = 0; k*acc).  A
-// skipped (insulated) face adds +0.0, which leaves acc unchanged because acc
-// is never -0.0 (it starts at +0.0 and round-to-nearest sums of nonzero terms
-// are never -0).  Fast mode uses ghost values (insulated: ghost = self; Robin:
-// ghost = x[i+1] - robin*self), one sum-then-subtract and folded constants.
+// in the order x-, x+, y-, y+, z-, z+, the Robin term at ix = 0, k*acc) and
+// integrate_step's stage arithmetic (acc + 2.0*k as an exact FMA).  Fast mode
+// uses ghost values, one sum-then-subtract and constants folded with k.
 #pragma once
+
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
 
 namespace pirk {
 
-constexpr int kHeatT = 32;                  // output tile edge (x and y)
-constexpr int kHeatH = 4;                   // halo = number of RK stages
+constexpr int kHeatT = 32;                 // output tile edge (x and y)
+constexpr int kHeatH = 4;                  // halo = number of RK stages
+constexpr int kHeatP = kHeatT + 2 * kHeatH;  // 40: pitch of every plane buffer
+constexpr int kHeatPlane = kHeatP * kHeatP;  // 1600
 constexpr int kHeatThreads = 512;
-constexpr int kHeatW0 = kHeatT + 2 * kHeatH;  // 40: loaded x plane edge
-constexpr int kHeatW1 = kHeatW0 - 2;          // 38: u1 plane edge
-constexpr int kHeatW2 = kHeatW0 - 4;          // 36
-constexpr int kHeatW3 = kHeatW0 - 6;          // 34
-constexpr int kHeatXRing = 6;                 // planes j-4 .. j+1
+constexpr int kHeatXRing = 5;              // x planes j-3 .. j+1
 constexpr int kHeatURing = 3;
-constexpr int kHeatARing = 4;
-
-constexpr size_t kHeatSmemDoubles =
-    size_t(kHeatXRing) * kHeatW0 * kHeatW0 + size_t(kHeatURing) * kHeatW1 * kHeatW1 +
-    size_t(kHeatURing) * kHeatW2 * kHeatW2 + size_t(kHeatURing) * kHeatW3 * kHeatW3 +
-    size_t(kHeatARing) * kHeatT * kHeatT;
-constexpr size_t kHeatSmemBytes = kHeatSmemDoubles * sizeof(double);
-
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+constexpr int kHeatLoads = (kHeatPlane + kHeatThreads - 1) / kHeatThreads;  // 4
+constexpr size_t kHeatSmemBytes =
+    size_t(kHeatXRing + 3 * kHeatURing) * kHeatPlane * sizeof(double);   // 179,200 B
 
 struct HeatStepParams {
     double kk, robin;
-    // fast-mode folded constants
-    double h2kk, hkk, h6kk;
+    double h2kk, hkk, h6kk;  // fast-mode folded constants
 };
 
-// One stencil evaluation.  Returns k (exact) or t = sum - 6 self with k = kk*t (fast).
-template <bool Exact>
-__device__ __forceinline__ double heat_point(double s, double xm, double xp, double ym, double yp,
-                                             double zm, double zp, bool hx_m, bool hx_p,
-                                             bool hy_m, bool hy_p, bool hz_m, bool hz_p,
-                                             double robin, double kk) {
+// face flags for edge tiles
+enum : int { kXm = 1, kXp = 2, kYm = 4, kYp = 8, kIn = 16 };
+
+// One stencil evaluation at level-0 offset `o` of plane c (neighbour planes
+// zm/zp, equal to c on an insulated z face).  Exact: returns k = kk*acc.
+// Fast: returns t = (sum of neighbours) - 6*self (k = kk*t is folded later).
+template <bool Exact, bool Interior>
+__device__ __forceinline__ double heat_eval(const double* __restrict__ c,
+                                            const double* __restrict__ zm,
+                                            const double* __restrict__ zp, int o, int flags,
+                                            const HeatStepParams& hp) {
+    const double s = c[o];
+    const double xm = c[o - 1], xp = c[o + 1];
+    const double ym = c[o - kHeatP], yp = c[o + kHeatP];
+    const double vzm = zm[o], vzp = zp[o];
     if constexpr (Exact) {
         double acc = 0.0;
-        acc += hx_m ? (xm - s) : ((xp - s) - robin * s);
-        acc += hx_p ? (xp - s) : 0.0;
-        acc += hy_m ? (ym - s) : 0.0;
-        acc += hy_p ? (yp - s) : 0.0;
-        acc += hz_m ? (zm - s) : 0.0;
-        acc += hz_p ? (zp - s) : 0.0;
-        return kk * acc;
+        if constexpr (Interior) {
+            acc += xm - s;
+            acc += xp - s;
+            acc += ym - s;
+            acc += yp - s;
+        } else {
+            acc += (flags & kXm) ? (xm - s) : ((xp - s) - hp.robin * s);
+            acc += (flags & kXp) ? (xp - s) : 0.0;
+            acc += (flags & kYm) ? (ym - s) : 0.0;
+            acc += (flags & kYp) ? (yp - s) : 0.0;
+        }
+        acc += vzm - s;
+        acc += vzp - s;
+        return hp.kk * acc;
     } else {
-        const double gxm = hx_m ? xm : fma(-robin, s, xp);
-        const double gxp = hx_p ? xp : s;
-        const double gym = hy_m ? ym : s;
-        const double gyp = hy_p ? yp : s;
-        const double gzm = hz_m ? zm : s;
-        const double gzp = hz_p ? zp : s;
-        const double sum = ((gxm + gxp) + (gym + gyp)) + (gzm + gzp);
+        double gxm = xm, gxp = xp, gym = ym, gyp = yp;
+        if constexpr (!Interior) {
+            gxm = (flags & kXm) ? xm : fma(-hp.robin, s, xp);
+            gxp = (flags & kXp) ? xp : s;
+            gym = (flags & kYm) ? ym : s;
+            gyp = (flags & kYp) ? yp : s;
+        }
+        const double sum = ((gxm + gxp) + (gym + gyp)) + (vzm + vzp);
         return fma(-6.0, s, sum);
+    }
+}
+
+struct HeatThread {
+    int own_off[2];     // level-0 offsets of the two own points
+    int own_flags[2];
+    int own_g[2];       // in-plane global offset iy*g + ix (valid iff flags & kIn)
+    int ring_off[3];    // level L = 1..3 halo-ring point (-1: none)
+    int ring_flags[3];
+    int ld_q[kHeatLoads];   // smem offset of each prefetched element (-1: none)
+    int ld_g[kHeatLoads];   // in-plane global offset
+};
+
+__device__ __forceinline__ int face_flags(long long ix, long long iy, long long g) {
+    int f = 0;
+    if (ix >= 0 && ix < g && iy >= 0 && iy < g) f |= kIn;
+    if (ix > 0) f |= kXm;
+    if (ix + 1 < g) f |= kXp;
+    if (iy > 0) f |= kYm;
+    if (iy + 1 < g) f |= kYp;
+    return f;
+}
+
+template <bool Exact, bool Interior>
+__device__ __forceinline__ void heat_stream(const HeatModel& m, const HeatStepParams& hp,
+                                            const WindowArgs& w, const StepConsts& sc,
+                                            unsigned long long step, unsigned long long* fail,
+                                            const HeatThread& th, double* smem, int field,
+                                            long long ob, long long oe) {
+    const long long g = static_cast<long long>(m.g);
+    const long long g2 = g * g;
+    double* sX = smem;
+    double* sU = smem + kHeatXRing * kHeatPlane;  // [level 1..3][ring 3][plane]
+    auto U = [&](int L, long long p) { return sU + ((L - 1) * kHeatURing + (p % kHeatURing)) * kHeatPlane; };
+    auto X = [&](long long p) { return sX + (p % kHeatXRing) * kHeatPlane; };
+
+    const long long zs = (ob - kHeatH > 0) ? ob - kHeatH : 0;
+    const long long ze = (oe + kHeatH < g) ? oe + kHeatH : g;
+    const long long lo_shift = (zs > 0) ? 1 : 0;
+    const long long hi_shift = (ze < g) ? 1 : 0;
+    const double* __restrict__ src = (field ? w.in1 : w.in0) - static_cast<long long>(w.win_begin) * g2;
+    double* __restrict__ dst = (field ? w.out1 : w.out0) - static_cast<long long>(w.out_begin) * g2;
+
+    double pre[kHeatLoads];
+    auto issue_loads = [&](long long p) {
+        const double* plane = src + p * g2;
+#pragma unroll
+        for (int i = 0; i < kHeatLoads; ++i)
+            if (th.ld_q[i] >= 0) pre[i] = __ldg(plane + th.ld_g[i]);
+    };
+    auto store_loads = [&](long long p) {
+        double* slot = X(p);
+#pragma unroll
+        for (int i = 0; i < kHeatLoads; ++i)
+            if (th.ld_q[i] >= 0) slot[th.ld_q[i]] = pre[i];
+    };
+
+    // register-resident per own point: x and accumulator of the planes in flight
+    double xr[2][4], ar[2][4];
+
+    issue_loads(zs);
+    store_loads(zs);
+
+    auto body = [&](long long j, auto phase_tag) {
+        constexpr int PH = decltype(phase_tag)::value;  // (j - zs) mod 4
+        __syncthreads();
+        const bool more = j + 1 < ze;
+        if (more) issue_loads(j + 1);
+
+        // ---- stage 1 at plane p = j - 1 (own + ring level 1)
+        {
+            const long long p = j - 1;
+            if (p >= zs + lo_shift && p < ze - hi_shift) {
+                const double* c = X(p);
+                const double* zm = (p > 0) ? X(p - 1) : c;
+                const double* zp = (p + 1 < g) ? X(p + 1) : c;
+                double* u = U(1, p);
+                constexpr int R = (PH + 3) & 3;  // register slot of plane j-1
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    if (!Interior && !(th.own_flags[k] & kIn)) continue;
+                    const int o = th.own_off[k];
+                    const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.own_flags[k], hp);
+                    const double x = c[o];
+                    xr[k][R] = x;
+                    ar[k][R] = kv;
+                    u[o] = Exact ? x + sc.h2 * kv : fma(hp.h2kk, kv, x);
+                }
+                const int o = th.ring_off[0];
+                if (o >= 0 && (Interior || (th.ring_flags[0] & kIn))) {
+                    const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.ring_flags[0], hp);
+                    u[o] = Exact ? c[o] + sc.h2 * kv : fma(hp.h2kk, kv, c[o]);
+                }
+            }
+        }
+        __syncthreads();
+        // ---- stages 2 and 3 at planes j - 2, j - 3
+#pragma unroll
+        for (int L = 2; L <= 3; ++L) {
+            const long long p = j - L;
+            if (p >= zs + L * lo_shift && p < ze - L * hi_shift) {
+                const double* c = U(L - 1, p);
+                const double* zm = (p > 0) ? U(L - 1, p - 1) : c;
+                const double* zp = (p + 1 < g) ? U(L - 1, p + 1) : c;
+                double* u = U(L, p);
+                const int R = (PH + 4 - L) & 3;
+                const double cs = (L == 2) ? sc.h2 : sc.hk;
+                const double cf = (L == 2) ? hp.h2kk : hp.hkk;
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    if (!Interior && !(th.own_flags[k] & kIn)) continue;
+                    const int o = th.own_off[k];
+                    const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.own_flags[k], hp);
+                    const double x = xr[k][R];
+                    ar[k][R] = fma(2.0, kv, ar[k][R]);  // acc + 2.0*k, exact (2k is exact)
+                    u[o] = Exact ? x + cs * kv : fma(cf, kv, x);
+                }
+                const int o = th.ring_off[L - 1];
+                if (o >= 0 && (Interior || (th.ring_flags[L - 1] & kIn))) {
+                    const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.ring_flags[L - 1], hp);
+                    const double x = X(p)[o];
+                    u[o] = Exact ? x + cs * kv : fma(cf, kv, x);
+                }
+            }
+            __syncthreads();
+        }
+        // ---- stage 4 at plane j - 4 (own points only), stored to HBM
+        {
+            const long long p = j - 4;
+            if (p >= ob && p < oe) {
+                const double* c = U(3, p);
+                const double* zm = (p > 0) ? U(3, p - 1) : c;
+                const double* zp = (p + 1 < g) ? U(3, p + 1) : c;
+                constexpr int R = PH & 3;  // (PH + 4 - 4)
+                double* out = dst + p * g2;
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    if (!Interior && !(th.own_flags[k] & kIn)) continue;
+                    const int o = th.own_off[k];
+                    const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.own_flags[k], hp);
+                    const double x = xr[k][R];
+                    const double xn = Exact ? x + sc.h6 * (ar[k][R] + kv) : fma(hp.h6kk, ar[k][R] + kv, x);
+                    out[th.own_g[k]] = xn;
+                    if (!finite_d(xn)) {
+                        const unsigned long long gi =
+                            static_cast<unsigned long long>(p * g2 + th.own_g[k]);
+                        if (m.method == 0)
+                            record_fail(fail, step, gi + (field ? static_cast<unsigned long long>(g2 * g) : 0ull));
+                        else if (fail)
+                            record_fail(fail + field, step, gi);
+                    }
+                }
+            }
+        }
+        // x plane j+1 replaces plane j-4, which no stage of this iteration read
+        if (more) store_loads(j + 1);
+    };
+
+    const long long jend = ze + kHeatH;
+    for (long long j = zs; j < jend; j += 4) {
+        body(j, std::integral_constant<int, 0>{});
+        if (j + 1 < jend) body(j + 1, std::integral_constant<int, 1>{});
+        if (j + 2 < jend) body(j + 2, std::integral_constant<int, 2>{});
+        if (j + 3 < jend) body(j + 3, std::integral_constant<int, 3>{});
     }
 }
 
@@ -93,143 +271,64 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
                  unsigned long long* __restrict__ fail) {
     (void)sizeof(ModeCheck<Exact>);
     extern __shared__ __align__(16) double smem[];
-    double* sX = smem;                                            // [6][40*40]
-    double* sU1 = sX + kHeatXRing * kHeatW0 * kHeatW0;            // [3][38*38]
-    double* sU2 = sU1 + kHeatURing * kHeatW1 * kHeatW1;           // [3][36*36]
-    double* sU3 = sU2 + kHeatURing * kHeatW2 * kHeatW2;           // [3][34*34]
-    double* sAcc = sU3 + kHeatURing * kHeatW3 * kHeatW3;          // [4][32*32]
-
     const int tid = threadIdx.x;
     const long long g = static_cast<long long>(m.g);
-    const long long g2 = g * g;
     const int field = blockIdx.z & 1;
     const long long chunk = blockIdx.z >> 1;
     const long long ix0 = static_cast<long long>(blockIdx.x) * kHeatT;
     const long long iy0 = static_cast<long long>(blockIdx.y) * kHeatT;
-
     const long long ob = static_cast<long long>(w.out_begin) + chunk * static_cast<long long>(zchunk);
     long long oe = ob + static_cast<long long>(zchunk);
     if (oe > static_cast<long long>(w.out_end)) oe = static_cast<long long>(w.out_end);
     if (ob >= oe) return;
-    // planes streamed through the CTA and the validity of each stage level
-    const long long zs = (ob - kHeatH > 0) ? ob - kHeatH : 0;
-    const long long ze = (oe + kHeatH < g) ? oe + kHeatH : g;
-    const long long lo_shift = (zs > 0) ? 1 : 0;
-    const long long hi_shift = (ze < g) ? 1 : 0;
 
-    const double* __restrict__ src = field ? w.in1 : w.in0;
-    double* __restrict__ dst = field ? w.out1 : w.out0;
-    const long long wb = static_cast<long long>(w.win_begin);
-
-    auto load_plane = [&](long long p) {
-        double* slot = sX + (p % kHeatXRing) * (kHeatW0 * kHeatW0);
-        const double* plane = src + (p - wb) * g2;
-        for (int q = tid; q < kHeatW0 * kHeatW0; q += kHeatThreads) {
-            const int y = q / kHeatW0, x = q - (q / kHeatW0) * kHeatW0;
-            const long long ix = ix0 - kHeatH + x, iy = iy0 - kHeatH + y;
-            if (ix >= 0 && ix < g && iy >= 0 && iy < g) cp_async8(slot + q, plane + iy * g + ix);
-        }
-        cp_async_commit();
-    };
-
-    load_plane(zs);
-
-    for (long long j = zs; j < ze + kHeatH; ++j) {
-        cp_async_wait_all();
-        __syncthreads();
-        if (j + 1 < ze) load_plane(j + 1);
-
-        // stages 1..4 at planes j-1 .. j-4
+    // ---- per-thread static assignment
+    HeatThread th;
+    {
+        const int ox = tid & 31, oy = tid >> 5;
 #pragma unroll
-        for (int L = 1; L <= 4; ++L) {
-            const long long p = j - L;
-            const bool valid = (p >= zs + L * lo_shift) && (p < ze - L * hi_shift) &&
-                               (L < 4 || (p >= ob && p < oe));
-            if (valid) {
-                const int Wd = kHeatW0 - 2 * L;      // this level's edge
-                const int Ws = Wd + 2;               // source level's edge
-                const int off = kHeatH - L;          // level origin relative to tile origin
-                const double* sp;                    // source ring
-                int sring;
-                if (L == 1) { sp = sX; sring = kHeatXRing; }
-                else if (L == 2) { sp = sU1; sring = kHeatURing; }
-                else if (L == 3) { sp = sU2; sring = kHeatURing; }
-                else { sp = sU3; sring = kHeatURing; }
-                const int splane = Ws * Ws;
-                const double* s_c = sp + (p % sring) * splane;
-                const double* s_m = (p > 0) ? sp + ((p - 1) % sring) * splane : s_c;
-                const double* s_p = (p + 1 < g) ? sp + ((p + 1) % sring) * splane : s_c;
-                const double* xc = sX + (p % kHeatXRing) * (kHeatW0 * kHeatW0);
-                double* ud = (L == 1) ? sU1 + (p % kHeatURing) * (kHeatW1 * kHeatW1)
-                           : (L == 2) ? sU2 + (p % kHeatURing) * (kHeatW2 * kHeatW2)
-                           : (L == 3) ? sU3 + (p % kHeatURing) * (kHeatW3 * kHeatW3)
-                                      : nullptr;
-                double* acc = sAcc + (p % kHeatARing) * (kHeatT * kHeatT);
-                const bool hz_m = p > 0, hz_p = p + 1 < g;
-                for (int q = tid; q < Wd * Wd; q += kHeatThreads) {
-                    const int y = q / Wd, x = q - (q / Wd) * Wd;
-                    const long long ix = ix0 - off + x, iy = iy0 - off + y;
-                    if (ix < 0 || ix >= g || iy < 0 || iy >= g) continue;
-                    const int si = (y + 1) * Ws + (x + 1);
-                    const double s = s_c[si];
-                    const double kv = heat_point<Exact>(
-                        s, s_c[si - 1], s_c[si + 1], s_c[si - Ws], s_c[si + Ws], s_m[si], s_p[si],
-                        ix > 0, ix + 1 < g, iy > 0, iy + 1 < g, hz_m, hz_p, hp.robin, hp.kk);
-                    const double xv = xc[(y + L) * kHeatW0 + (x + L)];  // level-L (x,y) is level-0 (x+L, y+L)
-                    const int ax = x - off, ay = y - off;  // accumulator coordinates
-                    const bool own = ax >= 0 && ax < kHeatT && ay >= 0 && ay < kHeatT;
-                    const int ai = ay * kHeatT + ax;
-                    if constexpr (Exact) {
-                        if (L == 1) {
-                            ud[q] = xv + sc.h2 * kv;
-                            if (own) acc[ai] = kv;
-                        } else if (L == 2) {
-                            ud[q] = xv + sc.h2 * kv;
-                            if (own) acc[ai] = acc[ai] + 2.0 * kv;
-                        } else if (L == 3) {
-                            ud[q] = xv + sc.hk * kv;
-                            if (own) acc[ai] = acc[ai] + 2.0 * kv;
-                        } else {
-                            const double xn = xv + sc.h6 * (acc[ai] + kv);
-                            const long long gi = ((p * g) + iy) * g + ix;
-                            dst[(p - static_cast<long long>(w.out_begin)) * g2 + iy * g + ix] = xn;
-                            if (!finite_d(xn)) {
-                                if (m.method == 0)
-                                    record_fail(fail, step, static_cast<unsigned long long>(gi) +
-                                                                (field ? static_cast<unsigned long long>(g2 * g) : 0ull));
-                                else if (fail)
-                                    record_fail(fail + field, step, static_cast<unsigned long long>(gi));
-                            }
-                        }
-                    } else {
-                        // kv is t = sum - 6 self; k = kk * t folded into the constants
-                        if (L == 1) {
-                            ud[q] = fma(hp.h2kk, kv, xv);
-                            if (own) acc[ai] = kv;
-                        } else if (L == 2) {
-                            ud[q] = fma(hp.h2kk, kv, xv);
-                            if (own) acc[ai] = fma(2.0, kv, acc[ai]);
-                        } else if (L == 3) {
-                            ud[q] = fma(hp.hkk, kv, xv);
-                            if (own) acc[ai] = fma(2.0, kv, acc[ai]);
-                        } else {
-                            const double xn = fma(hp.h6kk, acc[ai] + kv, xv);
-                            const long long gi = ((p * g) + iy) * g + ix;
-                            dst[(p - static_cast<long long>(w.out_begin)) * g2 + iy * g + ix] = xn;
-                            if (!finite_d(xn)) {
-                                if (m.method == 0)
-                                    record_fail(fail, step, static_cast<unsigned long long>(gi) +
-                                                                (field ? static_cast<unsigned long long>(g2 * g) : 0ull));
-                                else if (fail)
-                                    record_fail(fail + field, step, static_cast<unsigned long long>(gi));
-                            }
-                        }
-                    }
+        for (int k = 0; k < 2; ++k) {
+            const int y = oy + 16 * k;
+            th.own_off[k] = (y + kHeatH) * kHeatP + (ox + kHeatH);
+            const long long ix = ix0 + ox, iy = iy0 + y;
+            th.own_flags[k] = face_flags(ix, iy, g);
+            th.own_g[k] = static_cast<int>(iy * g + ix);
+        }
+#pragma unroll
+        for (int L = 1; L <= 3; ++L) {
+            const int hw = kHeatH - L, W = kHeatT + 2 * hw;
+            const int count = W * W - kHeatT * kHeatT;
+            th.ring_off[L - 1] = -1;
+            th.ring_flags[L - 1] = 0;
+            if (tid < count) {
+                int r = tid, x, y;
+                if (r < hw * W) { y = r / W; x = r % W; }
+                else if ((r -= hw * W) < hw * W) { y = W - hw + r / W; x = r % W; }
+                else { r -= hw * W; y = hw + r / (2 * hw); const int c = r % (2 * hw); x = (c < hw) ? c : kHeatT + c; }
+                th.ring_off[L - 1] = (y + L) * kHeatP + (x + L);
+                th.ring_flags[L - 1] = face_flags(ix0 - hw + x, iy0 - hw + y, g);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kHeatLoads; ++i) {
+            const int q = tid + i * kHeatThreads;
+            th.ld_q[i] = -1;
+            th.ld_g[i] = 0;
+            if (q < kHeatPlane) {
+                const long long ix = ix0 - kHeatH + q % kHeatP, iy = iy0 - kHeatH + q / kHeatP;
+                if (ix >= 0 && ix < g && iy >= 0 && iy < g) {
+                    th.ld_q[i] = q;
+                    th.ld_g[i] = static_cast<int>(iy * g + ix);
                 }
             }
-            if (L < 4) __syncthreads();
         }
     }
+    const bool interior = ix0 - kHeatH >= 0 && ix0 + kHeatT + kHeatH <= g && iy0 - kHeatH >= 0 &&
+                          iy0 + kHeatT + kHeatH <= g;
+    if (interior)
+        heat_stream<Exact, true>(m, hp, w, sc, step, fail, th, smem, field, ob, oe);
+    else
+        heat_stream<Exact, false>(m, hp, w, sc, step, fail, th, smem, field, ob, oe);
 }
 
 template <bool Exact>
@@ -254,14 +353,13 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
     const uint64_t planes = w.out_end - w.out_begin;
     // z chunks: enough CTAs to fill the machine, few enough to keep the
     // 8-plane halo overhead per chunk small.
-    const uint64_t tiles = ((m.g + kHeatT - 1) / kHeatT) * ((m.g + kHeatT - 1) / kHeatT);
+    const uint64_t tx = (m.g + kHeatT - 1) / kHeatT;
     uint64_t nchunks = 1;
-    while (tiles * 2 * nchunks < 4 * 148 && planes / (nchunks * 2) >= 64) nchunks *= 2;
+    while (tx * tx * 2 * nchunks < 4 * 148 && planes / (nchunks * 2) >= 64) nchunks *= 2;
     const uint64_t zchunk = (planes + nchunks - 1) / nchunks;
     nchunks = (planes + zchunk - 1) / zchunk;
-    const unsigned tx = static_cast<unsigned>((m.g + kHeatT - 1) / kHeatT);
-    dim3 grid(tx, tx, static_cast<unsigned>(2 * nchunks)), block(kHeatThreads);
-    heat_step_kernel<Exact><<<grid, block, kHeatSmemBytes, stream>>>(m, hp, w, sc, step, zchunk, fail);
+    dim3 grid(static_cast<unsigned>(tx), static_cast<unsigned>(tx), static_cast<unsigned>(2 * nchunks));
+    heat_step_kernel<Exact><<<grid, kHeatThreads, kHeatSmemBytes, stream>>>(m, hp, w, sc, step, zchunk, fail);
     return cudaGetLastError();
 }
 
