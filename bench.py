@@ -1,0 +1,414 @@
+"""Benchmark of the PIRK reachability hot path on B200.
+
+Default workload (BASELINE.json config 5 / north-star target): CTMM
+(mixed monotonicity) of heat3d with grid = 1600 (n = 4.096e9, embedding state
+2n = 8.19e9 fp64), h = 5e-8, strong-scaled over N GPUs as z-slabs with NCCL
+halo exchange.  One bench "step" is one RK4 step of the whole embedding.
+
+* value  -- state-updates/s (2n per step) with the state resident in HBM,
+            CUDA events on the launching stream, max over ranks.
+* e2e    -- the same metric through the public API (paper_2001_10635_b200.
+            mixed_monotonicity, host buffers in and out, H2D/D2H in the timed
+            region) for the full 100-step C5 reach.
+* roofline, cpu_baseline (the reference itself, oracle/_ref, on this host),
+  clocks, gpu_launches -- see DESIGN.md.
+
+``--impl reference`` times the reference's own CPU implementation (oracle/_ref,
+built from /root/reference/proj/src) on bounded samples of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RK4 state-updates/sec (2n*steps/s), CTMM heat3d n=4.096e9"
+UNIT = "state-updates/s"
+GRID = 1600
+H = 5e-8
+C5_STEPS = 100
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------- our arm
+
+def heat_device_bench(args, world, rank, local, torch, pk, dist):
+    """Device-resident CTMM steps of heat3d (sharded z-slabs for N > 1)."""
+    from paper_2001_10635_b200 import sharded as S
+
+    model = pk.make_heat3d(args.grid)
+    ctx = pk.Context(local, args.mode)
+    K = 1
+    shard = S.Shard(args.grid, world, rank, 4 * K)
+    unit = args.grid * args.grid
+    ex = S.HaloExchanger(shard, unit) if world > 1 else None
+    step_fn = S.device_step_fn(model, "mixed-monotonicity", ctx)
+    run = S.ShardedReach(model, "mixed-monotonicity", shard, step_fn, ex, K=K)
+    dev = torch.device("cuda", local)
+    a = run.alloc(lambda n: torch.empty(n, dtype=torch.float64, device=dev))
+    a[0].fill_(0.9)  # catalog default box [0.9, 1.1] (models.cpp:744-745)
+    a[1].fill_(1.1)
+    steps = [(float(k) * args.h, args.h) for k in range(args.warmup + args.steps)]
+    launches0 = ctx.launch_count()
+    run.run(steps[: args.warmup], 0)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        l0 = ctx.launch_count()
+        ev0.record(stream)
+        run.run(steps[args.warmup:], args.warmup)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        l1 = ctx.launch_count()
+        if world > 1:
+            dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    # sanity: finite result (cheap device reduction)
+    ok = bool(torch.isfinite(a[0]).all().item()) if args.check else True
+    del a, run
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    ctx.close()
+    return ms_max, l1 - l0, clk.summary(), ok, launches0
+
+
+def heat_e2e(args, pk, torch, world):
+    """Full C5 reach (100 steps, final set) through the public API with host
+    buffers; H2D of the initial box and D2H of the final box are timed."""
+    import psutil
+
+    g = args.grid
+    n = g ** 3
+    need = 4 * n * 8
+    avail = psutil.virtual_memory().available
+    if need > 0.75 * avail:
+        # keep the box alive: scale the e2e grid down rather than exhaust host RAM
+        g = int(round((0.75 * avail / 32) ** (1.0 / 3.0)))
+        n = g ** 3
+    # page-locked host buffers via cudaHostRegister (torch's pinned allocator
+    # rounds requests up to powers of two, which would not fit host RAM here)
+    bufs = [np.empty(n) for _ in range(4)]
+    cudart = torch.cuda.cudart()
+    for b in bufs:
+        cudart.cudaHostRegister(b.ctypes.data, b.nbytes, 0)
+    lo, hi, olo, ohi = bufs
+    lo.fill(0.9)
+    hi.fill(1.1)
+    model = pk.make_heat3d(g)
+    # IntervalVector validation is part of problem construction (interval.cpp:10-23),
+    # outside the reference's mixed_monotonicity call; done before timing here too.
+    prob = pk.ReachProblem(model, pk.IntervalVector(lo, hi), None, 0.0,
+                           C5_STEPS * args.h, args.h, 0)
+    ctx = pk.get_context(0)
+    ctx.set_mode(args.mode)
+    t0 = time.perf_counter()
+    tube = pk.mixed_monotonicity(prob, ctx=ctx, out=(olo, ohi))
+    dt = time.perf_counter() - t0
+    steps = tube.report.steps
+    res = {"value": 2.0 * n * steps / dt, "unit": UNIT, "h2d_bytes_per_step": 2 * n * 8,
+           "d2h_bytes_per_step": 2 * n * 8, "seconds": dt, "rk4_steps": steps,
+           "n": n, "grid": g, "api": "paper_2001_10635_b200.mixed_monotonicity",
+           "step": "one full C5 reach call (H2D initial box, 100 RK4 steps, order check, D2H final box)"}
+    ok = bool(np.isfinite(olo[:: max(1, n // 4096)]).all())
+    del tube, prob, lo, hi, olo, ohi
+    for b in bufs:
+        cudart.cudaHostUnregister(b.ctypes.data)
+    del bufs
+    return res, ok
+
+
+def cpu_baseline(args):
+    """The reference itself (oracle/_ref) on this host, bounded sample."""
+    from oracle import oracle as O
+
+    import paper_2001_10635_b200 as pk
+
+    if not O.ref_available():
+        return None
+    g, steps = args.cpu_grid, args.cpu_steps
+    model = pk.make_heat3d(g)
+    n = g ** 3
+    threads = O.ref_max_threads()
+    r = O.ref_reach(O.METHOD_MM, model, np.full(n, 0.9), np.full(n, 1.1), None, None, 0.0,
+                    steps * args.h, args.h, 0, workers=threads, keep=False)
+    rate = 2.0 * n * steps / r.report["integration_s"]
+    return {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"ivreach::mixed_monotonicity (oracle/_ref, -O3, OpenMP) heat3d grid={g} "
+                      f"(n={n}), {steps} RK4 steps, h={args.h}; rate = 2n*steps/integration_s",
+            "wall_s": r.wall_s}
+
+
+def secondary(args, pk, torch):
+    """Other BASELINE configs on one GPU (quick lines, not the headline)."""
+    out = {}
+    ctx = pk.get_context(0)
+    ctx.set_mode(args.mode)
+
+    def engine_rate(prob, steps=20):
+        eng = pk.Engine(prob, ctx=ctx)
+        stream = torch.cuda.Stream()
+        ctx.set_stream(stream.cuda_stream)
+        eng.advance(3)
+        eng.status()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.advance(steps)
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        eng.close()
+        ctx.set_stream(None)
+        return 2.0 * prob.model.dim / (ms * 1e-3), ms
+
+    # C3: traffic n=1e6 CTMM
+    n = 10 ** 6
+    m = pk.make_traffic(n)
+    p = pk.ReachProblem(m, pk.IntervalVector(np.full(n, 10.0), np.full(n, 20.0)),
+                        pk.IntervalVector([4.0], [6.0]), 0.0, 30.0, 0.5, 0)
+    v, ms = engine_rate(p, 40)
+    out["C3_traffic_ctmm_n1e6"] = {"value": v, "unit": UNIT, "ms_per_step": ms}
+    # C4: coupled chain n=1e7 (SDMM interpretation)
+    n = 10 ** 7
+    m = pk.make_chain(n)
+    c = 2.0 * np.random.default_rng(7).random(n) - 1.0
+    p = pk.ReachProblem(m, pk.IntervalVector(c - 0.05, c + 0.05), pk.IntervalVector([-0.1], [0.1]),
+                        0.0, 1.0, 0.01, 0)
+    v, ms = engine_rate(p, 40)
+    out["C4_chain_sdmm_n1e7"] = {"value": v, "unit": UNIT, "ms_per_step": ms}
+    # C2: arch-quadrotor Monte Carlo, m = 1e6, 100 steps
+    mq = pk.make_arch_quadrotor()
+    lo = np.array([-0.4] * 6 + [0.0] * 6)
+    p = pk.ReachProblem(mq, pk.IntervalVector(lo, -lo), None, 0.0, 1.0, 0.01, 0)
+    spec = pk.MonteCarloSpec(seed=1, samples_override=10 ** 6)
+    pk.monte_carlo(p, pk.MonteCarloSpec(seed=1, samples_override=10 ** 5), ctx=ctx)
+    t0 = time.perf_counter()
+    tube = pk.monte_carlo(p, spec, ctx=ctx)
+    dt = time.perf_counter() - t0
+    out["C2_archquad_mc_m1e6"] = {"value": 1e6 * tube.report.steps / dt, "unit": "sample-steps/s",
+                                  "kernel_s": tube.report.phases.integration_s,
+                                  "kernel_value": 1e6 * tube.report.steps / tube.report.phases.integration_s}
+    return out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2001_10635_b200 as pk
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    pk.set_default_mode(args.mode)
+    ms, launches, clocks, ok, _ = heat_device_bench(args, world, rank, local, torch, pk, dist)
+    n = args.grid ** 3
+    updates = 2.0 * n * args.steps
+    value = updates / (ms * 1e-3)
+    hbm, how = peaks()
+    per_launch_ms = ms / max(1, launches // max(1, world)) if launches else ms / args.steps
+    # dominant kernel: heat_step_kernel, one launch per step per rank
+    launch_bytes = 16.0 * 2 * n / world
+    achieved = launch_bytes / (per_launch_ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "heat_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tj = json.load(f).get(args.mode)
+        if tj:
+            traffic = tj["dram_bytes_per_update"] * 2 * n / world
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"CTMM heat3d grid={args.grid} (n={n}), embedding 2n, "
+                               f"h={args.h}, z-slab sharded with NCCL halo exchange",
+                   "mode": args.mode, "grid": args.grid, "n": n, "state_bytes": 32 * n,
+                   "l2": "inputs (65.5 GB) far larger than the 126 MB L2; no flush needed",
+                   "parallelism": f"zslab{world}"},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic, "peak_source": how,
+                     "kernel": "heat_step_kernel", "algorithmic_bytes_per_launch": launch_bytes,
+                     "avg_launch_ms": per_launch_ms},
+        "finite": ok,
+    }
+    if rank == 0 and not args.no_e2e and world == 1:
+        e2e, ok2 = heat_e2e(args, pk, torch, world)
+        line["e2e"] = e2e
+        line["finite"] = line["finite"] and ok2
+    elif rank == 0 and not args.no_e2e:
+        line["e2e"] = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(args)
+    if rank == 0 and world == 1 and not args.no_secondary:
+        line["secondary"] = secondary(args, pk, torch)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------- reference arm
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    import paper_2001_10635_b200 as pk
+
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libivreach_ref.so not built"}))
+        return
+    g, per = args.cpu_grid, args.ref_steps_per_call
+    model = pk.make_heat3d(g)
+    n = g ** 3
+    lo, hi = np.full(n, 0.9), np.full(n, 1.1)
+    threads = O.ref_max_threads()
+    rates, secs = [], 0.0
+    for i in range(args.warmup + args.steps):
+        r = O.ref_reach(O.METHOD_MM, model, lo, hi, None, None, 0.0, per * args.h, args.h, 0,
+                        workers=threads, keep=False)
+        if i >= args.warmup:
+            secs += r.report["integration_s"]
+            rates.append(2.0 * n * per / r.report["integration_s"])
+    value = 2.0 * n * per * args.steps / secs
+    sample = (f"ivreach::mixed_monotonicity heat3d grid={g} (n={n}), {per} RK4 steps per call, "
+              f"h={args.h}; rate = 2n*steps/integration_s (the C5 grid=1600 needs 459 GB on CPU)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"CTMM heat3d (bounded sample grid={g} of the grid={GRID} workload)",
+                       "parallelism": f"openmp{threads}"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="fast", choices=["fast", "exact"])
+    ap.add_argument("--grid", type=int, default=GRID)
+    ap.add_argument("--h", type=float, default=H)
+    ap.add_argument("--cpu-grid", type=int, default=300)
+    ap.add_argument("--cpu-steps", type=int, default=10)
+    ap.add_argument("--ref-steps-per-call", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--check", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

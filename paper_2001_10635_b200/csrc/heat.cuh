@@ -45,11 +45,9 @@ constexpr int kHeatH = 4;                  // halo = number of RK stages
 constexpr int kHeatP = kHeatT + 2 * kHeatH;  // 40: pitch of every plane buffer
 constexpr int kHeatPlane = kHeatP * kHeatP;  // 1600
 constexpr int kHeatThreads = 512;
-constexpr int kHeatXRing = 5;              // x planes j-3 .. j+1
-constexpr int kHeatURing = 3;
+constexpr int kHeatRing = 4;               // planes per ring (x, u1, u2, u3)
 constexpr int kHeatLoads = (kHeatPlane + kHeatThreads - 1) / kHeatThreads;  // 4
-constexpr size_t kHeatSmemBytes =
-    size_t(kHeatXRing + 3 * kHeatURing) * kHeatPlane * sizeof(double);   // 179,200 B
+constexpr size_t kHeatSmemBytes = size_t(4 * kHeatRing) * kHeatPlane * sizeof(double);  // 204,800 B
 
 struct HeatStepParams {
     double kk, robin;
@@ -120,148 +118,187 @@ __device__ __forceinline__ int face_flags(long long ix, long long iy, long long 
     return f;
 }
 
+// Shared-memory rings: 4 slots per level (x, u1, u2, u3), slot of plane p =
+// (p - zs) mod 4.  With the plane loop unrolled by 4, every slot offset below
+// is a compile-time immediate.
+template <int PH, int Back>
+__device__ __forceinline__ constexpr int heat_slot(int level) {
+    return (level * kHeatRing + ((PH - Back + 8) & 3)) * kHeatPlane;
+}
+
+template <bool Exact, bool Interior, int PH>
+__device__ __forceinline__ void heat_iteration(const HeatModel& m, const HeatStepParams& hp,
+                                               const StepConsts& sc, unsigned long long step,
+                                               unsigned long long* fail, const HeatThread& th,
+                                               double* __restrict__ smem, int field, int j,
+                                               int zs, int ze, int ob, int oe, int lo_shift,
+                                               int hi_shift, int g, long long g2,
+                                               const double* __restrict__ src,
+                                               double* __restrict__ dst, double (&xr)[2][4],
+                                               double (&ar)[2][4], double (&pre)[kHeatLoads]) {
+    __syncthreads();
+    const bool more = j + 1 < ze;
+    if (more) {
+        const double* plane = src + static_cast<long long>(j + 1) * g2;
+#pragma unroll
+        for (int i = 0; i < kHeatLoads; ++i)
+            if (th.ld_q[i] >= 0) pre[i] = __ldg(plane + th.ld_g[i]);
+    }
+
+    // ---- stage 1 at plane p = j - 1 (own points + level-1 ring point)
+    {
+        const int p = j - 1;
+        if (p >= zs + lo_shift && p < ze - hi_shift) {
+            const double* c = smem + heat_slot<PH, 1>(0);
+            const double* zm = (p > 0) ? smem + heat_slot<PH, 2>(0) : c;
+            const double* zp = (p + 1 < g) ? smem + heat_slot<PH, 0>(0) : c;
+            double* u = smem + heat_slot<PH, 1>(1);
+            constexpr int R = (PH + 3) & 3;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                if (!Interior && !(th.own_flags[k] & kIn)) continue;
+                const int o = th.own_off[k];
+                const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.own_flags[k], hp);
+                const double x = c[o];
+                xr[k][R] = x;
+                ar[k][R] = kv;
+                u[o] = Exact ? x + sc.h2 * kv : fma(hp.h2kk, kv, x);
+            }
+            const int o = th.ring_off[0];
+            if (o >= 0 && (Interior || (th.ring_flags[0] & kIn))) {
+                const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.ring_flags[0], hp);
+                u[o] = Exact ? c[o] + sc.h2 * kv : fma(hp.h2kk, kv, c[o]);
+            }
+        }
+    }
+    __syncthreads();
+    // ---- stage 2 at plane j - 2
+    {
+        const int p = j - 2;
+        if (p >= zs + 2 * lo_shift && p < ze - 2 * hi_shift) {
+            const double* c = smem + heat_slot<PH, 2>(1);
+            const double* zm = (p > 0) ? smem + heat_slot<PH, 3>(1) : c;
+            const double* zp = (p + 1 < g) ? smem + heat_slot<PH, 1>(1) : c;
+            double* u = smem + heat_slot<PH, 2>(2);
+            constexpr int R = (PH + 2) & 3;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                if (!Interior && !(th.own_flags[k] & kIn)) continue;
+                const int o = th.own_off[k];
+                const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.own_flags[k], hp);
+                const double x = xr[k][R];
+                ar[k][R] = fma(2.0, kv, ar[k][R]);  // acc + 2.0*k (exact: 2k is exact)
+                u[o] = Exact ? x + sc.h2 * kv : fma(hp.h2kk, kv, x);
+            }
+            const int o = th.ring_off[1];
+            if (o >= 0 && (Interior || (th.ring_flags[1] & kIn))) {
+                const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.ring_flags[1], hp);
+                const double x = smem[heat_slot<PH, 2>(0) + o];
+                u[o] = Exact ? x + sc.h2 * kv : fma(hp.h2kk, kv, x);
+            }
+        }
+    }
+    __syncthreads();
+    // ---- stage 3 at plane j - 3
+    {
+        const int p = j - 3;
+        if (p >= zs + 3 * lo_shift && p < ze - 3 * hi_shift) {
+            const double* c = smem + heat_slot<PH, 3>(2);
+            const double* zm = (p > 0) ? smem + heat_slot<PH, 4>(2) : c;
+            const double* zp = (p + 1 < g) ? smem + heat_slot<PH, 2>(2) : c;
+            double* u = smem + heat_slot<PH, 3>(3);
+            constexpr int R = (PH + 1) & 3;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                if (!Interior && !(th.own_flags[k] & kIn)) continue;
+                const int o = th.own_off[k];
+                const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.own_flags[k], hp);
+                const double x = xr[k][R];
+                ar[k][R] = fma(2.0, kv, ar[k][R]);
+                u[o] = Exact ? x + sc.hk * kv : fma(hp.hkk, kv, x);
+            }
+            const int o = th.ring_off[2];
+            if (o >= 0 && (Interior || (th.ring_flags[2] & kIn))) {
+                const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.ring_flags[2], hp);
+                const double x = smem[heat_slot<PH, 3>(0) + o];
+                u[o] = Exact ? x + sc.hk * kv : fma(hp.hkk, kv, x);
+            }
+        }
+    }
+    __syncthreads();
+    // x plane j+1 takes the slot of plane j-3, dead after stage 3
+    if (more) {
+        double* slot = smem + heat_slot<PH, 3>(0);
+#pragma unroll
+        for (int i = 0; i < kHeatLoads; ++i)
+            if (th.ld_q[i] >= 0) slot[th.ld_q[i]] = pre[i];
+    }
+    // ---- stage 4 at plane j - 4 (own points only), stored to HBM
+    {
+        const int p = j - 4;
+        if (p >= ob && p < oe) {
+            const double* c = smem + heat_slot<PH, 4>(3);
+            const double* zm = (p > 0) ? smem + heat_slot<PH, 5>(3) : c;
+            const double* zp = (p + 1 < g) ? smem + heat_slot<PH, 3>(3) : c;
+            constexpr int R = PH & 3;
+            double* out = dst + static_cast<long long>(p) * g2;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                if (!Interior && !(th.own_flags[k] & kIn)) continue;
+                const int o = th.own_off[k];
+                const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.own_flags[k], hp);
+                const double x = xr[k][R];
+                const double xn =
+                    Exact ? x + sc.h6 * (ar[k][R] + kv) : fma(hp.h6kk, ar[k][R] + kv, x);
+                out[th.own_g[k]] = xn;
+                if (!finite_d(xn)) {
+                    const unsigned long long gi = static_cast<unsigned long long>(
+                        static_cast<long long>(p) * g2 + th.own_g[k]);
+                    if (m.method == 0)
+                        record_fail(fail, step,
+                                    gi + (field ? static_cast<unsigned long long>(g2 * g) : 0ull));
+                    else if (fail)
+                        record_fail(fail + field, step, gi);
+                }
+            }
+        }
+    }
+}
+
 template <bool Exact, bool Interior>
 __device__ __forceinline__ void heat_stream(const HeatModel& m, const HeatStepParams& hp,
                                             const WindowArgs& w, const StepConsts& sc,
                                             unsigned long long step, unsigned long long* fail,
                                             const HeatThread& th, double* smem, int field,
-                                            long long ob, long long oe) {
-    const long long g = static_cast<long long>(m.g);
-    const long long g2 = g * g;
-    double* sX = smem;
-    double* sU = smem + kHeatXRing * kHeatPlane;  // [level 1..3][ring 3][plane]
-    auto U = [&](int L, long long p) { return sU + ((L - 1) * kHeatURing + (p % kHeatURing)) * kHeatPlane; };
-    auto X = [&](long long p) { return sX + (p % kHeatXRing) * kHeatPlane; };
-
-    const long long zs = (ob - kHeatH > 0) ? ob - kHeatH : 0;
-    const long long ze = (oe + kHeatH < g) ? oe + kHeatH : g;
-    const long long lo_shift = (zs > 0) ? 1 : 0;
-    const long long hi_shift = (ze < g) ? 1 : 0;
-    const double* __restrict__ src = (field ? w.in1 : w.in0) - static_cast<long long>(w.win_begin) * g2;
+                                            int ob, int oe) {
+    const int g = static_cast<int>(m.g);
+    const long long g2 = static_cast<long long>(g) * g;
+    const int zs = (ob - kHeatH > 0) ? ob - kHeatH : 0;
+    const int ze = (oe + kHeatH < g) ? oe + kHeatH : g;
+    const int lo_shift = (zs > 0) ? 1 : 0;
+    const int hi_shift = (ze < g) ? 1 : 0;
+    const double* __restrict__ src =
+        (field ? w.in1 : w.in0) - static_cast<long long>(w.win_begin) * g2;
     double* __restrict__ dst = (field ? w.out1 : w.out0) - static_cast<long long>(w.out_begin) * g2;
 
-    double pre[kHeatLoads];
-    auto issue_loads = [&](long long p) {
-        const double* plane = src + p * g2;
+    double xr[2][4], ar[2][4], pre[kHeatLoads];
+    {  // plane zs -> x slot 0
+        const double* plane = src + static_cast<long long>(zs) * g2;
 #pragma unroll
         for (int i = 0; i < kHeatLoads; ++i)
-            if (th.ld_q[i] >= 0) pre[i] = __ldg(plane + th.ld_g[i]);
-    };
-    auto store_loads = [&](long long p) {
-        double* slot = X(p);
-#pragma unroll
-        for (int i = 0; i < kHeatLoads; ++i)
-            if (th.ld_q[i] >= 0) slot[th.ld_q[i]] = pre[i];
-    };
-
-    // register-resident per own point: x and accumulator of the planes in flight
-    double xr[2][4], ar[2][4];
-
-    issue_loads(zs);
-    store_loads(zs);
-
-    auto body = [&](long long j, auto phase_tag) {
-        constexpr int PH = decltype(phase_tag)::value;  // (j - zs) mod 4
-        __syncthreads();
-        const bool more = j + 1 < ze;
-        if (more) issue_loads(j + 1);
-
-        // ---- stage 1 at plane p = j - 1 (own + ring level 1)
-        {
-            const long long p = j - 1;
-            if (p >= zs + lo_shift && p < ze - hi_shift) {
-                const double* c = X(p);
-                const double* zm = (p > 0) ? X(p - 1) : c;
-                const double* zp = (p + 1 < g) ? X(p + 1) : c;
-                double* u = U(1, p);
-                constexpr int R = (PH + 3) & 3;  // register slot of plane j-1
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    if (!Interior && !(th.own_flags[k] & kIn)) continue;
-                    const int o = th.own_off[k];
-                    const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.own_flags[k], hp);
-                    const double x = c[o];
-                    xr[k][R] = x;
-                    ar[k][R] = kv;
-                    u[o] = Exact ? x + sc.h2 * kv : fma(hp.h2kk, kv, x);
-                }
-                const int o = th.ring_off[0];
-                if (o >= 0 && (Interior || (th.ring_flags[0] & kIn))) {
-                    const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.ring_flags[0], hp);
-                    u[o] = Exact ? c[o] + sc.h2 * kv : fma(hp.h2kk, kv, c[o]);
-                }
-            }
-        }
-        __syncthreads();
-        // ---- stages 2 and 3 at planes j - 2, j - 3
-#pragma unroll
-        for (int L = 2; L <= 3; ++L) {
-            const long long p = j - L;
-            if (p >= zs + L * lo_shift && p < ze - L * hi_shift) {
-                const double* c = U(L - 1, p);
-                const double* zm = (p > 0) ? U(L - 1, p - 1) : c;
-                const double* zp = (p + 1 < g) ? U(L - 1, p + 1) : c;
-                double* u = U(L, p);
-                const int R = (PH + 4 - L) & 3;
-                const double cs = (L == 2) ? sc.h2 : sc.hk;
-                const double cf = (L == 2) ? hp.h2kk : hp.hkk;
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    if (!Interior && !(th.own_flags[k] & kIn)) continue;
-                    const int o = th.own_off[k];
-                    const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.own_flags[k], hp);
-                    const double x = xr[k][R];
-                    ar[k][R] = fma(2.0, kv, ar[k][R]);  // acc + 2.0*k, exact (2k is exact)
-                    u[o] = Exact ? x + cs * kv : fma(cf, kv, x);
-                }
-                const int o = th.ring_off[L - 1];
-                if (o >= 0 && (Interior || (th.ring_flags[L - 1] & kIn))) {
-                    const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.ring_flags[L - 1], hp);
-                    const double x = X(p)[o];
-                    u[o] = Exact ? x + cs * kv : fma(cf, kv, x);
-                }
-            }
-            __syncthreads();
-        }
-        // ---- stage 4 at plane j - 4 (own points only), stored to HBM
-        {
-            const long long p = j - 4;
-            if (p >= ob && p < oe) {
-                const double* c = U(3, p);
-                const double* zm = (p > 0) ? U(3, p - 1) : c;
-                const double* zp = (p + 1 < g) ? U(3, p + 1) : c;
-                constexpr int R = PH & 3;  // (PH + 4 - 4)
-                double* out = dst + p * g2;
-#pragma unroll
-                for (int k = 0; k < 2; ++k) {
-                    if (!Interior && !(th.own_flags[k] & kIn)) continue;
-                    const int o = th.own_off[k];
-                    const double kv = heat_eval<Exact, Interior>(c, zm, zp, o, th.own_flags[k], hp);
-                    const double x = xr[k][R];
-                    const double xn = Exact ? x + sc.h6 * (ar[k][R] + kv) : fma(hp.h6kk, ar[k][R] + kv, x);
-                    out[th.own_g[k]] = xn;
-                    if (!finite_d(xn)) {
-                        const unsigned long long gi =
-                            static_cast<unsigned long long>(p * g2 + th.own_g[k]);
-                        if (m.method == 0)
-                            record_fail(fail, step, gi + (field ? static_cast<unsigned long long>(g2 * g) : 0ull));
-                        else if (fail)
-                            record_fail(fail + field, step, gi);
-                    }
-                }
-            }
-        }
-        // x plane j+1 replaces plane j-4, which no stage of this iteration read
-        if (more) store_loads(j + 1);
-    };
-
-    const long long jend = ze + kHeatH;
-    for (long long j = zs; j < jend; j += 4) {
-        body(j, std::integral_constant<int, 0>{});
-        if (j + 1 < jend) body(j + 1, std::integral_constant<int, 1>{});
-        if (j + 2 < jend) body(j + 2, std::integral_constant<int, 2>{});
-        if (j + 3 < jend) body(j + 3, std::integral_constant<int, 3>{});
+            if (th.ld_q[i] >= 0) smem[th.ld_q[i]] = __ldg(plane + th.ld_g[i]);
     }
+    const int jend = ze + kHeatH;
+#define PIRK_HEAT_IT(PH)                                                                        \
+    heat_iteration<Exact, Interior, PH>(m, hp, sc, step, fail, th, smem, field, j + PH, zs, ze, \
+                                        ob, oe, lo_shift, hi_shift, g, g2, src, dst, xr, ar, pre)
+    for (int j = zs; j < jend; j += 4) {
+        PIRK_HEAT_IT(0);
+        if (j + 1 < jend) PIRK_HEAT_IT(1);
+        if (j + 2 < jend) PIRK_HEAT_IT(2);
+        if (j + 3 < jend) PIRK_HEAT_IT(3);
+    }
+#undef PIRK_HEAT_IT
 }
 
 template <bool Exact>
@@ -326,9 +363,11 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
     const bool interior = ix0 - kHeatH >= 0 && ix0 + kHeatT + kHeatH <= g && iy0 - kHeatH >= 0 &&
                           iy0 + kHeatT + kHeatH <= g;
     if (interior)
-        heat_stream<Exact, true>(m, hp, w, sc, step, fail, th, smem, field, ob, oe);
+        heat_stream<Exact, true>(m, hp, w, sc, step, fail, th, smem, field,
+                                  static_cast<int>(ob), static_cast<int>(oe));
     else
-        heat_stream<Exact, false>(m, hp, w, sc, step, fail, th, smem, field, ob, oe);
+        heat_stream<Exact, false>(m, hp, w, sc, step, fail, th, smem, field,
+                                  static_cast<int>(ob), static_cast<int>(oe));
 }
 
 template <bool Exact>

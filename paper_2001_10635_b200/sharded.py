@@ -1,0 +1,201 @@
+"""State-sharded (multi-GPU) mixed-monotonicity / growth-bound runs and
+sample-sharded Monte Carlo, one process per GPU.
+
+* 1-D chains (traffic, coupled chain) shard contiguous component ranges;
+  heat3d shards contiguous z-slabs (``i = ix + g*iy + g^2*iz`` makes a slab a
+  contiguous block, models.cpp:110-112).  Each rank keeps a window of its
+  units plus a halo of ``4*K`` units per side and exchanges halos every ``K``
+  RK4 steps (deep halos: the 4-stage dependency cone shrinks the valid window
+  by 4 units per step).  Every owned unit is computed from exactly the inputs
+  a single-device run uses, so the result is bit-identical for any rank count.
+* Monte Carlo shards the sample index range; the counter-based RNG needs no
+  communication, and the hull is combined with one MIN and one MAX
+  all-reduce (exact, order-independent).
+
+The driver is executor-agnostic: ``step_fn`` performs one windowed RK4 step
+(on a B200 it is :func:`device_step_fn`, the CUDA kernel through the C ABI)
+and ``comm`` moves halo units between neighbours (NCCL point-to-point on
+GPUs; the tests drive the same code over gloo).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+
+from .models import HEAT3D, SystemModel
+
+
+def units_of(model: SystemModel):
+    """(number of partition units, components per unit)."""
+    if model.kind == HEAT3D:
+        return model.grid, model.grid * model.grid
+    return model.dim, 1
+
+
+@dataclass
+class Shard:
+    """Rank-local partition of ``units`` with a halo of ``halo`` units."""
+
+    units: int
+    world: int
+    rank: int
+    halo: int
+
+    @property
+    def begin(self) -> int:
+        return self.units * self.rank // self.world
+
+    @property
+    def end(self) -> int:
+        return self.units * (self.rank + 1) // self.world
+
+    @property
+    def win_begin(self) -> int:
+        return max(self.begin - self.halo, 0)
+
+    @property
+    def win_end(self) -> int:
+        return min(self.end + self.halo, self.units)
+
+    @property
+    def win_len(self) -> int:
+        return self.win_end - self.win_begin
+
+    def out_range(self, s: int):
+        """Units computable at sub-step s (0-based) after a halo exchange."""
+        shrink = 4 * (s + 1)
+        lo = self.win_begin if self.win_begin == 0 else self.win_begin + shrink
+        hi = self.win_end if self.win_end == self.units else self.win_end - shrink
+        return lo, hi
+
+
+def plan_rk4_steps(t0: float, t1: float, h: float):
+    """(t, hk) per step: rk4.cpp:8-17 and :99-100, in float64 like the host engine."""
+    span = t1 - t0
+    full = int(np.floor(span / h + 1e-9))
+    rem = span - float(full) * h
+    total = full + (1 if rem > 1e-9 * h else 0)
+    out = []
+    for k in range(total):
+        t = t0 + float(k) * h
+        hk = (t1 - t) if k + 1 == total else h
+        out.append((t, hk))
+    return out
+
+
+class HaloExchanger:
+    """Sends the rank's boundary units to its neighbours and receives theirs,
+    over torch.distributed point-to-point (NCCL on GPUs, gloo in tests)."""
+
+    def __init__(self, shard: Shard, unit: int, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.shard = shard
+        self.unit = unit
+        self.group = group
+
+    def exchange(self, fields):
+        """fields: list of 1-D tensors of length win_len*unit (window layout)."""
+        s = self.shard
+        H = s.halo
+        u = self.unit
+        ops = []
+        left, right = s.rank - 1, s.rank + 1
+        wb = s.win_begin
+        recv = []
+        for f in fields:
+            if left >= 0:
+                snd = f[(s.begin - wb) * u:(s.begin - wb + H) * u].contiguous()
+                rcv = f.new_empty((s.begin - s.win_begin) * u)
+                ops.append(self.dist.P2POp(self.dist.isend, snd, left, self.group))
+                ops.append(self.dist.P2POp(self.dist.irecv, rcv, left, self.group))
+                recv.append((f, 0, rcv))
+            if right < s.world:
+                snd = f[(s.end - wb - H) * u:(s.end - wb) * u].contiguous()
+                rcv = f.new_empty((s.win_end - s.end) * u)
+                ops.append(self.dist.P2POp(self.dist.isend, snd, right, self.group))
+                ops.append(self.dist.P2POp(self.dist.irecv, rcv, right, self.group))
+                recv.append((f, (s.end - wb) * u, rcv))
+        if ops:
+            for r in self.dist.batch_isend_irecv(ops):
+                r.wait()
+        for f, off, rcv in recv:
+            f[off:off + rcv.numel()].copy_(rcv)
+
+
+def device_step_fn(model: SystemModel, method: str, ctx=None):
+    """Windowed RK4 step on the B200 (pirk_step_window on torch tensors)."""
+    from .reach import get_context, step_window
+
+    ctx = ctx or get_context()
+
+    def step(in0, in1, out0, out1, win_begin, win_len, out_begin, out_end, p0, p1, t, hk, k,
+             fail_ptr=0):
+        import torch
+
+        ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        # out pointers address unit out_begin inside the window buffers
+        unit = units_of(model)[1]
+        off = (out_begin - win_begin) * unit * 8
+        step_window(model, method, in0.data_ptr(), in1.data_ptr(), out0.data_ptr() + off,
+                    out1.data_ptr() + off, win_begin, win_len, out_begin, out_end, p0, p1, t, hk,
+                    k, fail_ptr, ctx=ctx)
+    return step
+
+
+class ShardedReach:
+    """Runs the RK4 step loop of one shard: window buffers (two fields,
+    ping-pong), ``K``-step deep halos.  Tensors may live on any torch device
+    the ``step_fn`` understands."""
+
+    def __init__(self, model: SystemModel, method: str, shard: Shard, step_fn: Callable,
+                 exchanger: Optional[HaloExchanger], p0=None, p1=None, K: int = 1):
+        assert shard.halo == 4 * K, "halo must be 4*K units for K steps between exchanges"
+        self.model = model
+        self.method = method
+        self.shard = shard
+        self.step_fn = step_fn
+        self.ex = exchanger
+        self.p0, self.p1 = p0, p1
+        self.K = K
+        self.unit = units_of(model)[1]
+
+    def alloc(self, like_tensor_factory):
+        n = self.shard.win_len * self.unit
+        self.a = [like_tensor_factory(n), like_tensor_factory(n)]
+        self.b = [like_tensor_factory(n), like_tensor_factory(n)]
+        return self.a
+
+    def run(self, steps, k0: int = 0):
+        """steps: list of (t, hk) for global step indices k0, k0+1, ..."""
+        s = self.shard
+        for i, (t, hk) in enumerate(steps):
+            sub = (k0 + i) % self.K
+            if sub == 0 and self.ex is not None and s.world > 1:
+                self.ex.exchange(self.a)
+            lo, hi = s.out_range(sub)
+            self.step_fn(self.a[0], self.a[1], self.b[0], self.b[1], s.win_begin, s.win_len,
+                         lo, hi, self.p0, self.p1, t, hk, k0 + i)
+            self.a, self.b = self.b, self.a
+
+    def owned(self):
+        s = self.shard
+        u = self.unit
+        o0 = (s.begin - s.win_begin) * u
+        o1 = (s.end - s.win_begin) * u
+        return self.a[0][o0:o1], self.a[1][o0:o1]
+
+
+def mc_sample_range(m: int, world: int, rank: int):
+    return m * rank // world, m * (rank + 1) // world
+
+
+def allreduce_hull(lower, upper, group=None):
+    """Combine per-rank Monte Carlo hulls (torch tensors): exact MIN/MAX."""
+    import torch.distributed as dist
+
+    dist.all_reduce(lower, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(upper, op=dist.ReduceOp.MAX, group=group)
