@@ -305,3 +305,42 @@ def test_missing_capabilities_rejected(ctx):
     prob2 = pk.ReachProblem(ll, pk.IntervalVector(np.zeros(7), np.ones(7)), None, 0.0, 1.0, 0.1, 0)
     with pytest.raises(ValueError, match="no decomposition"):
         pk.mixed_monotonicity(prob2, ctx=ctx)
+
+
+# ------------------------------------------- golden vectors from the reference
+
+GOLDEN = __import__("os").path.join(__import__("os").path.dirname(__file__), "golden", "golden.npz")
+
+
+def _golden_cases():
+    from tests.golden.make_golden import cases
+    return cases()
+
+
+@pytest.mark.parametrize("case", _golden_cases(), ids=lambda c: c[0])
+def test_cuda_matches_reference_golden(ctx, case):
+    """The CUDA path against vectors produced by the reference itself."""
+    name, method, model, lo, hi, plo, phi, t0, t1, h, stride, kw = case
+    g = np.load(GOLDEN)
+
+    class R:
+        times = g[f"{name}__times"]
+        lower = g[f"{name}__lower"]
+        upper = g[f"{name}__upper"]
+
+    n = model.dim
+    init = pk.IntervalVector(np.broadcast_to(np.asarray(lo, float), (n,)),
+                             np.broadcast_to(np.asarray(hi, float), (n,)))
+    inputs = pk.IntervalVector(plo, phi) if plo is not None else None
+    prob = pk.ReachProblem(model, init, inputs, t0, t1, h, stride)
+    if method == O.METHOD_MM:
+        tube = pk.mixed_monotonicity(prob, ctx=ctx)
+    elif method == O.METHOD_GB:
+        tube = pk.growth_bound(prob, ctx=ctx)
+    else:
+        tube = pk.monte_carlo(prob, pk.MonteCarloSpec(seed=kw["seed"], samples_override=kw["samples"]),
+                              ctx=ctx)
+    if model.kind == pk.ARCH_QUAD:  # CUDA sin/cos vs glibc: tolerance contract
+        assert_within(tube, R, rel=1e-12, atol=1e-14, never_tighter=(method != O.METHOD_MC))
+    else:
+        assert_bitexact(tube, R)

@@ -1,0 +1,163 @@
+"""CPU, multi-process (gloo): the sharded driver used for N > 1 GPUs.
+
+Each rank runs paper_2001_10635_b200.sharded.ShardedReach on its slab with
+deep halos exchanged by HaloExchanger (torch.distributed point-to-point),
+exactly as on NCCL; here the per-step executor is the oracle's windowed RK4
+step (test infrastructure), which reads NaN outside its window so any halo
+bug poisons the result.  The gathered result must be bit-identical to the
+single-process oracle run (SURVEY.md 8e invariant: k-GPU == 1-GPU)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2001_10635_b200 as pk
+from oracle import oracle as O
+from paper_2001_10635_b200 import sharded as S
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def oracle_step_fn(model, method):
+    meth = 0 if method == "mixed-monotonicity" else 1
+    unit = S.units_of(model)[1]
+
+    def step(in0, in1, out0, out1, wb, wl, lo, hi, p0, p1, t, hk, k):
+        o0, o1 = O.step_window(model, meth, in0.numpy(), in1.numpy(), wb, wl, lo, hi, p0, p1, t,
+                               hk)
+        a = (lo - wb) * unit
+        out0[a:a + o0.size] = torch.from_numpy(o0)
+        out1[a:a + o1.size] = torch.from_numpy(o1)
+    return step
+
+
+def problem(kind):
+    if kind == "traffic":
+        m = pk.make_traffic(301)
+        lo = 10.0 + (np.arange(301) % 7)
+        return m, "mixed-monotonicity", lo, lo + 5.0, [4.0], [6.0], 0.0, 6.0, 0.5
+    if kind == "traffic_gb":
+        m = pk.make_traffic(301)
+        lo = 10.0 + (np.arange(301) % 7)
+        return m, "growth-bound", lo, lo + 5.0, [4.0], [6.0], 0.0, 6.0, 0.5
+    if kind == "chain":
+        m = pk.make_chain(257)
+        c = 2.0 * np.array([O.u01(7, 0, i) for i in range(257)]) - 1.0
+        return m, "mixed-monotonicity", c - 0.05, c + 0.05, [-0.1], [0.1], 0.0, 0.1, 0.01
+    m = pk.make_heat3d(26)
+    n = m.dim
+    lo = 0.9 - 0.05 * ((np.arange(n) * 7) % 5)
+    return m, "mixed-monotonicity", lo, lo + 0.2, None, None, 0.0, 0.003, 0.0003
+
+
+def worker(rank, world, port, kind, K, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m, method, lo, hi, plo, phi, t0, t1, h = problem(kind)
+        units, unit = S.units_of(m)
+        shard = S.Shard(units, world, rank, 4 * K)
+        if method == "growth-bound":
+            c0, r0 = 0.5 * (hi + lo), 0.5 * (hi - lo)
+            p0 = [0.5 * (phi[0] + plo[0])]
+            p1 = [0.5 * (phi[0] - plo[0])]
+            f0, f1 = c0, r0
+        else:
+            f0, f1, p0, p1 = lo, hi, plo, phi
+        ex = S.HaloExchanger(shard, unit)
+        run = S.ShardedReach(m, method, shard, oracle_step_fn(m, method), ex, p0, p1, K=K)
+        a = run.alloc(lambda n: torch.full((n,), float("nan"), dtype=torch.float64))
+        sl = slice(shard.win_begin * unit, shard.win_end * unit)
+        a[0].copy_(torch.from_numpy(np.ascontiguousarray(f0[sl])))
+        a[1].copy_(torch.from_numpy(np.ascontiguousarray(f1[sl])))
+        run.run(S.plan_rk4_steps(t0, t1, h), 0)
+        o0, o1 = run.owned()
+        q.put((rank, shard.begin * unit, o0.numpy().copy(), o1.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,world,K", [("traffic", 2, 1), ("traffic", 3, 2), ("chain", 2, 1),
+                                          ("chain", 3, 3), ("heat", 2, 1), ("heat", 3, 1),
+                                          ("traffic_gb", 2, 2)])
+def test_sharded_equals_single(kind, world, K):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, world, port, kind, K, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    m, method, lo, hi, plo, phi, t0, t1, h = problem(kind)
+    fn = O.mixed_monotonicity if method == "mixed-monotonicity" else O.growth_bound
+    ref = fn(m, lo, hi, plo, phi, t0, t1, h, 0)
+    n = m.dim
+    g0 = np.full(n, np.nan)
+    g1 = np.full(n, np.nan)
+    for _, off, o0, o1 in parts:
+        g0[off:off + o0.size] = o0
+        g1[off:off + o1.size] = o1
+    if method == "growth-bound":  # box epilogue (reach.cpp:121-134)
+        r = np.where((g1 < 0) & (g1 >= -1e-12), 0.0, g1)
+        g0, g1 = g0 - r, g0 + r
+    assert np.array_equal(g0, ref.lower[-1]) and np.array_equal(g1, ref.upper[-1])
+
+
+def mc_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = pk.make_laub_loomis()
+        c = np.array([1.2, 1.05, 1.5, 2.4, 1.0, 0.1, 0.45])
+        s0, s1 = S.mc_sample_range(1000, world, rank)
+        r = O.monte_carlo(m, c - 0.05, c + 0.05, None, None, 0.0, 0.5, 0.005, 20, 9, 1000, s0, s1)
+        lo, hi = torch.from_numpy(r.lower.copy()), torch.from_numpy(r.upper.copy())
+        S.allreduce_hull(lo, hi)
+        q.put((rank, lo.numpy(), hi.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_mc_sample_sharding_allreduce():
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=mc_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    m = pk.make_laub_loomis()
+    c = np.array([1.2, 1.05, 1.5, 2.4, 1.0, 0.1, 0.45])
+    ref = O.monte_carlo(m, c - 0.05, c + 0.05, None, None, 0.0, 0.5, 0.005, 20, 9, 1000)
+    for _, lo, hi in parts:
+        assert np.array_equal(lo, ref.lower) and np.array_equal(hi, ref.upper)
+
+
+def test_shard_geometry():
+    for units, world, halo in [(1600, 8, 4), (1000, 3, 8), (26, 3, 4)]:
+        covered = []
+        for r in range(world):
+            s = S.Shard(units, world, r, halo)
+            assert s.win_begin <= s.begin < s.end <= s.win_end
+            lo, hi = s.out_range(halo // 4 - 1)
+            assert lo <= s.begin and hi >= s.end
+            covered.extend(range(s.begin, s.end))
+        assert covered == list(range(units))
