@@ -132,11 +132,13 @@ def heat_device_bench(args, world, rank, local, torch, pk, dist):
     a[1].fill_(1.1)
     steps = [(float(k) * args.h, args.h) for k in range(args.warmup + args.steps)]
     launches0 = ctx.launch_count()
-    run.run(steps[: args.warmup], 0)
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream(device=dev)  # kernels and events share this stream
+    with torch.cuda.stream(stream):
+        run.run(steps[: args.warmup], 0)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    stream = torch.cuda.current_stream()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -144,9 +146,10 @@ def heat_device_bench(args, world, rank, local, torch, pk, dist):
         if world > 1:
             dist.barrier()
         l0 = ctx.launch_count()
-        ev0.record(stream)
-        run.run(steps[args.warmup:], args.warmup)
-        ev1.record(stream)
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            run.run(steps[args.warmup:], args.warmup)
+            ev1.record(stream)
         torch.cuda.synchronize()
         l1 = ctx.launch_count()
         if world > 1:
@@ -396,7 +399,7 @@ def main():
     ap.add_argument("--h", type=float, default=H)
     ap.add_argument("--cpu-grid", type=int, default=300)
     ap.add_argument("--cpu-steps", type=int, default=10)
-    ap.add_argument("--ref-steps-per-call", type=int, default=2)
+    ap.add_argument("--ref-steps-per-call", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")

@@ -148,7 +148,8 @@ void pirk_destroy(pirk_ctx* ctx);
 const char* pirk_last_error(const pirk_ctx* ctx);
 pirk_status pirk_set_mode(pirk_ctx* ctx, int32_t mode);
 /* Launch on this cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
- * NULL restores the context's own stream. */
+ * NULL is the CUDA default stream.  pirk_get_stream right after pirk_create
+ * returns the context's own (non-blocking) stream. */
 pirk_status pirk_set_stream(pirk_ctx* ctx, void* stream);
 void* pirk_get_stream(pirk_ctx* ctx);
 uint64_t pirk_launch_count(const pirk_ctx* ctx);

@@ -874,7 +874,7 @@ pirk_status pirk_set_mode(pirk_ctx* ctx, int32_t mode) {
 
 pirk_status pirk_set_stream(pirk_ctx* ctx, void* stream) {
     if (!ctx) return PIRK_EINVAL;
-    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    ctx->stream = static_cast<cudaStream_t>(stream);  // NULL = the CUDA default stream
     return PIRK_OK;
 }
 

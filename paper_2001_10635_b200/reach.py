@@ -222,6 +222,7 @@ class Context:
                                "(no CUDA device?)")
         self._h = h
         self.device = int(device)
+        self._own_stream = L.pirk_get_stream(h)
         self.set_mode(mode)
 
     @property
@@ -234,7 +235,11 @@ class Context:
         self.mode = mode
 
     def set_stream(self, stream_ptr: Optional[int]) -> None:
-        self.check(_lib.lib().pirk_set_stream(self._h, C.c_void_p(stream_ptr or 0)))
+        """Launch on cudaStream_t ``stream_ptr`` (0 = the CUDA default stream);
+        None restores the context's own stream."""
+        if stream_ptr is None:
+            stream_ptr = self._own_stream
+        self.check(_lib.lib().pirk_set_stream(self._h, C.c_void_p(stream_ptr)))
 
     def launch_count(self) -> int:
         return int(_lib.lib().pirk_launch_count(self._h))
