@@ -6,27 +6,30 @@
 // (growth_rhs == rhs for heat3d, models.cpp:130).
 //
 // Design: 2.5-D z-streaming with register-resident z histories.
-//   A CTA of 256 threads owns a 32x32 x-y tile of one field and streams the
-//   planes of a z-chunk.  Iteration j loads x-plane j+1 (tile + halo 4) and
-//   evaluates stage 1 at plane j-1, stage 2 at j-2, stage 3 at j-3 and stage 4
-//   (the RK4 combination, stored to HBM) at j-4.  Every (x, y) column of the
-//   40x40 footprint is owned by one thread for the whole run, so the values of
-//   a column at neighbouring planes (the z+-1 terms, the RK accumulator, x for
-//   the stage updates) live in that thread's registers.  Shared memory only
-//   carries the in-plane (x+-1, y+-1) exchange: two planes per level (x, u1,
-//   u2, u3), each stage reading the plane its predecessor wrote in the
-//   previous iteration -- so one __syncthreads per plane, no intra-plane
-//   barriers.  Own points are 2x2 register blocks (inner neighbours from
-//   registers; 6 shared loads per block per stage), halo-ring columns are
-//   single points with up to three per thread.  HBM sees each x once and each
-//   x' once: 16 B per state-update.
+//   A CTA of 512 threads owns a 32x32 x-y tile of one field and streams the
+//   planes of a z-chunk.  Iteration j issues cp.async loads of x-plane j+1
+//   (tile + halo 4) into a 4-slot shared ring and evaluates stage 1 at plane
+//   j-1, stage 2 at j-2, stage 3 at j-3 and stage 4 (the RK4 combination,
+//   stored to HBM) at j-4.  Every (x, y) column of the 40x40 footprint belongs
+//   to one thread for the whole run, so a column's values at neighbouring
+//   planes (the z+-1 terms), its RK accumulator and its x for the stage
+//   updates stay in that thread's registers.  Shared memory carries only the
+//   in-plane (x+-1, y+-1) exchange: u1/u2/u3 planes double-buffered, each
+//   stage reading the plane its predecessor wrote in the previous iteration --
+//   one __syncthreads per plane.  Rows have an odd pitch (41 doubles) with
+//   even and odd columns de-interleaved, so both row-wise and column-wise
+//   neighbour loads of a warp are bank-conflict free.  Own points are 1x2
+//   register pairs (the pair's inner neighbours come from registers); the 576
+//   halo-ring columns are single points (one or two per thread).  HBM sees
+//   each x once and each x' once: 16 B per state-update.
 //
 // Boundaries.  Interior tiles (halo-4 footprint inside the grid in x and y)
-// run without per-point checks.  Insulated z faces use the centre value as
-// the missing neighbour: the term (s - s) = +0.0 leaves the running sum
-// exactly as skipping it does (the sum is never -0.0: it starts at +0.0 and
-// round-to-nearest sums of nonzero terms are never -0).  Edge tiles use
-// per-column face flags; exact mode then evaluates models.cpp:113-126
+// run without per-point checks.  Insulated z faces: the history slot of the
+// missing plane (-1 or g) holds the boundary plane's value, so the term
+// (s - s) = +0.0 leaves the running sum exactly as skipping it does (the sum
+// is never -0.0: it starts at +0.0 and round-to-nearest sums of nonzero terms
+// are never -0); these iterations are peeled off the main loop.  Edge tiles
+// use per-column face flags; exact mode then evaluates models.cpp:113-126
 // literally (Robin term at ix = 0).
 //
 // Exact mode follows the reference's expression order (acc = 0.0; acc += ...
@@ -35,8 +38,6 @@
 // constants folded with k.
 #pragma once
 
-#include <type_traits>
-
 #include "common.cuh"
 #include "kernels.h"
 
@@ -44,19 +45,22 @@ namespace pirk {
 
 constexpr int kHeatT = 32;                   // output tile edge (x and y)
 constexpr int kHeatH = 4;                    // halo = number of RK stages
-constexpr int kHeatP = kHeatT + 2 * kHeatH;  // 40: pitch of every plane buffer
-constexpr int kHeatPlane = kHeatP * kHeatP;  // 1600
-constexpr int kHeatThreads = 256;            // one 2x2 own block per thread
-constexpr int kHeatRingSlots = 3;            // halo columns per thread (576 <= 3*256)
-constexpr size_t kHeatSmemBytes = size_t(8) * kHeatPlane * sizeof(double);  // 102,400 B
+constexpr int kHeatW = kHeatT + 2 * kHeatH;  // 40: footprint edge
+constexpr int kHeatHalf = kHeatW / 2;        // 20: even / odd column sub-rows
+constexpr int kHeatP = kHeatW + 1;           // 41: odd row pitch (bank-conflict free)
+constexpr int kHeatPlane = kHeatW * kHeatP;  // 1640
+constexpr int kHeatThreads = 512;            // one 1x2 own pair per thread
+constexpr int kHeatXRing = 8;                // x planes j-4 .. j+1 (slot (p - zs) & 7)
+constexpr int kHeatPlanes = kHeatXRing + 3 * 2;  // + u1/u2/u3 double buffers
+constexpr size_t kHeatSmemBytes = size_t(kHeatPlanes) * kHeatPlane * sizeof(double);  // 183,680 B
 
 struct HeatStepParams {
     double kk, robin;
     double h2kk, hkk, h6kk;  // fast-mode folded constants
 };
 
-// face flags (edge tiles)
-enum : int { kXm = 1, kXp = 2, kYm = 4, kYp = 8, kIn = 16 };
+// face flags (edge tiles); kOdd marks an odd footprint column (neighbour offsets)
+enum : int { kXm = 1, kXp = 2, kYm = 4, kYp = 8, kIn = 16, kOdd = 32 };
 
 __device__ __forceinline__ int face_flags(long long ix, long long iy, long long g) {
     int f = 0;
@@ -67,6 +71,24 @@ __device__ __forceinline__ int face_flags(long long ix, long long iy, long long 
     if (iy + 1 < g) f |= kYp;
     return f;
 }
+
+// shared index of footprint column (x, y)
+__device__ __forceinline__ int heat_sidx(int x, int y) {
+    return y * kHeatP + (x & 1) * kHeatHalf + (x >> 1);
+}
+
+// buffer bases: x ring slot s (0..7); level L (1..3) parity par
+__device__ __forceinline__ constexpr int xbuf(int s) { return s * kHeatPlane; }
+__device__ __forceinline__ constexpr int ubuf(int L, int par) {
+    return (kHeatXRing + 2 * (L - 1) + par) * kHeatPlane;
+}
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 // Stencil value from the six neighbours.  Exact: k = kk*acc.  Fast: t = sum - 6 s.
 template <bool Exact, bool Interior>
@@ -101,17 +123,14 @@ __device__ __forceinline__ double heat_pt(double s, double xm, double xp, double
     }
 }
 
-// smem offset (in doubles) of level L's slot for plane parity `par`
-__device__ __forceinline__ constexpr int lvl(int L, int par) { return (2 * L + par) * kHeatPlane; }
-
 struct HeatCols {
-    int ob;                   // own 2x2 block: smem offset of its top-left column
-    int og[4];                // in-plane global offsets (iy*g + ix): (x,y), (x+1,y), (x,y+1), (x+1,y+1)
-    int of[4];                // face flags
-    int ro[kHeatRingSlots];   // halo-ring columns: smem offset (-1: none)
-    int rg[kHeatRingSlots];
-    int rf[kHeatRingSlots];
-    int rd[kHeatRingSlots];   // number of stages computed at the column (0..3; -1: none)
+    int oe;        // shared index of the pair's even column (the odd one is oe + 20)
+    int og;        // in-plane global offset of the even column (odd: og + 1)
+    int of[2];     // face flags of the two own columns
+    int ro[2];     // halo-ring columns: shared index
+    int rg[2];     // in-plane global offset
+    int rf[2];     // face flags (| kOdd)
+    int rd[2];     // number of stages computed at the column (0..3; -1: none)
 };
 
 template <bool Exact, bool Interior>
@@ -129,197 +148,182 @@ struct HeatRun {
     unsigned long long* fail;
     unsigned long long n_total;
 
-    // register state: slot (p - zs) & 3 of plane p; prefetch by parity
-    double ox[4][4], opre[4][2], ou1[4][4], ou2[4][4], ou3[4][4], oacc[4][4];
-    double r0x[4], r0pre[2], r0u1[4], r0u2[4];   // ring slot 0 (depth <= 3)
-    double r1x[4], r1pre[2], r1u1[4];            // ring slot 1 (depth <= 2)
-    double r2pre[2];                              // ring slot 2 (depth 0: load only)
+    // register state: slot (p - zs) & 3 of plane p
+    double ox[2][4], ou1[2][4], ou2[2][4], ou3[2][4], oacc[2][4];
+    double rx[4], ru1[4], ru2[4];   // ring slot 0 (depth <= 3)
 
     __device__ __forceinline__ bool in(int k) const { return Interior || (c.of[k] & kIn); }
 
-    __device__ __forceinline__ void load(int p, int par) {
+    // x(p) of this thread's columns: global -> shared x-ring slot s (async)
+    __device__ __forceinline__ void load(int p, int s) {
         const double* plane = src + static_cast<long long>(p) * g2;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (in(k)) opre[k][par] = __ldg(plane + c.og[k]);
-        if (c.rd[0] >= 0) r0pre[par] = __ldg(plane + c.rg[0]);
-        if (c.rd[1] >= 0) r1pre[par] = __ldg(plane + c.rg[1]);
-        if (c.rd[2] >= 0) r2pre[par] = __ldg(plane + c.rg[2]);
+        double* X = S + xbuf(s);
+        if (in(0)) cp_async8(X + c.oe, plane + c.og);
+        if (in(1)) cp_async8(X + c.oe + kHeatHalf, plane + c.og + 1);
+        if (c.rd[0] >= 0) cp_async8(X + c.ro[0], plane + c.rg[0]);
+        if (c.rd[1] >= 0) cp_async8(X + c.ro[1], plane + c.rg[1]);
+        cp_async_commit();
     }
 
-    __device__ __forceinline__ void store_x(int par_slot, int par_pre) {
-        double* X = S + lvl(0, par_slot);
-        *reinterpret_cast<double2*>(X + c.ob) = make_double2(opre[0][par_pre], opre[1][par_pre]);
-        *reinterpret_cast<double2*>(X + c.ob + kHeatP) = make_double2(opre[2][par_pre], opre[3][par_pre]);
-        if (c.rd[0] >= 0) X[c.ro[0]] = r0pre[par_pre];
-        if (c.rd[1] >= 0) X[c.ro[1]] = r1pre[par_pre];
-        if (c.rd[2] >= 0) X[c.ro[2]] = r2pre[par_pre];
+    // own pair: centres c0 (even col) and c1 (odd col) at level L-1 of plane p,
+    // z neighbours, in-plane neighbours from the shared buffer at `in_off`
+    __device__ __forceinline__ void pair_eval(double c0, double c1, double zm0, double zm1,
+                                              double zp0, double zp1, int in_off, double& k0,
+                                              double& k1) const {
+        const double* B = S + in_off;
+        const int e = c.oe, o = c.oe + kHeatHalf;
+        const double l = B[o - 1];            // (X0-1, Y): odd column of the previous pair
+        const double r = B[e + 1];            // (X0+2, Y): even column of the next pair
+        const double u0 = B[e - kHeatP], u1 = B[o - kHeatP];
+        const double d0 = B[e + kHeatP], d1 = B[o + kHeatP];
+        k0 = heat_pt<Exact, Interior>(c0, l, c1, u0, d0, zm0, zp0, c.of[0], hp);
+        k1 = heat_pt<Exact, Interior>(c1, c0, r, u1, d1, zm1, zp1, c.of[1], hp);
     }
 
-    // Own 2x2 block at level L-1: centres ctr[4], z neighbours zm/zp[4],
-    // in-plane neighbours from shared slot `in_off`.
-    __device__ __forceinline__ void block_eval(const double* ctr, const double* zm, const double* zp,
-                                               int in_off, double* kv) const {
-        const double* B = S + in_off + c.ob;
-        const double l0 = B[-1], l1 = B[kHeatP - 1];
-        const double r0 = B[2], r1 = B[kHeatP + 2];
-        const double2 up = *reinterpret_cast<const double2*>(B - kHeatP);
-        const double2 dn = *reinterpret_cast<const double2*>(B + 2 * kHeatP);
-        kv[0] = heat_pt<Exact, Interior>(ctr[0], l0, ctr[1], up.x, ctr[2], zm[0], zp[0], c.of[0], hp);
-        kv[1] = heat_pt<Exact, Interior>(ctr[1], ctr[0], r0, up.y, ctr[3], zm[1], zp[1], c.of[1], hp);
-        kv[2] = heat_pt<Exact, Interior>(ctr[2], l1, ctr[3], ctr[0], dn.x, zm[2], zp[2], c.of[2], hp);
-        kv[3] = heat_pt<Exact, Interior>(ctr[3], ctr[2], r1, ctr[1], dn.y, zm[3], zp[3], c.of[3], hp);
+    __device__ __forceinline__ double ring_eval(double s, double zm, double zp, int in_off) const {
+        const double* B = S + in_off + c.ro[0];
+        const int dm = (c.rf[0] & kOdd) ? -kHeatHalf : kHeatHalf - 1;  // offset of x-1
+        const double xm = B[dm], xp = B[dm + 1];                      // x+1 is the next slot
+        return heat_pt<Exact, Interior>(s, xm, xp, B[-kHeatP], B[kHeatP], zm, zp, c.rf[0], hp);
     }
 
-    __device__ __forceinline__ void block_store(int out_off, const double* v) const {
-        double* B = S + out_off + c.ob;
-        *reinterpret_cast<double2*>(B) = make_double2(v[0], v[1]);
-        *reinterpret_cast<double2*>(B + kHeatP) = make_double2(v[2], v[3]);
+    __device__ __forceinline__ double upd(double x, double k, double ce, double cf) const {
+        return Exact ? x + ce * k : fma(cf, k, x);
     }
 
-    __device__ __forceinline__ double ring_eval(int o, int f, double s, double zm, double zp,
-                                                int in_off) const {
-        const double* B = S + in_off + o;
-        return heat_pt<Exact, Interior>(s, B[-1], B[1], B[-kHeatP], B[kHeatP], zm, zp, f, hp);
-    }
-
-    template <int PH>
+    // ZEdge: the iteration touches an insulated z face (planes -1 or g)
+    template <int PH, bool ZEdge>
     __device__ __forceinline__ void iteration(int j) {
-        // register slots of planes j, j-1, j-2, j-3 (j-4 shares j's slot)
+        // register/x-ring slots of planes j, j-1, j-2, j-3 (j-4 shares j's, j-5 shares j-1's)
         constexpr int I0 = PH & 3, I1 = (PH + 3) & 3, I2 = (PH + 2) & 3, I3 = (PH + 1) & 3;
         constexpr int P0 = PH & 1, P1 = (PH + 1) & 1;  // parities of j and j-1
-        const bool more = j + 1 < ze;
-        if (more) load(j + 1, P1);      // x(j+1) -> prefetch[parity of j+1]
-        if (j < ze) store_x(P0, P0);    // x(j) -> shared, read by stage 1 of iteration j+1
+        const int x8 = (j - zs) & 7;                   // x-ring slot of plane j
+        const int X0 = xbuf(x8), X1 = xbuf((x8 + 7) & 7), X3 = xbuf((x8 + 5) & 7),
+                  X4 = xbuf((x8 + 4) & 7);
+        if (j + 1 < ze) load(j + 1, (x8 + 1) & 7);  // slot of x(j-7): no longer read
+        // own x(j) (arrived last iteration): the z+ neighbour of stage 1
+        double xj0 = S[X0 + c.oe], xj1 = S[X0 + c.oe + kHeatHalf];
+        double rxj = S[X0 + c.ro[0]];
+        if (ZEdge && j == g) {  // insulated top face: x(g) := x(g-1)
+            xj0 = ox[0][I1];
+            xj1 = ox[1][I1];
+            rxj = rx[I1];
+        }
 
         // ---------------- stage 1 at plane p = j-1
         {
             const int p = j - 1;
             if (p >= zs + lo_shift && p < ze - hi_shift) {
-                const bool hm = p > 0, hpz = p + 1 < g;
-                double ctr[4], zm[4], zp[4], kv[4], u[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    ctr[k] = ox[k][I1];
-                    zm[k] = hm ? ox[k][I2] : ctr[k];
-                    zp[k] = hpz ? opre[k][P0] : ctr[k];
+                double k0, k1;
+                pair_eval(ox[0][I1], ox[1][I1], ox[0][I2], ox[1][I2], xj0, xj1, X1, k0, k1);
+                const double u0 = upd(ox[0][I1], k0, sc.h2, hp.h2kk);
+                const double u1 = upd(ox[1][I1], k1, sc.h2, hp.h2kk);
+                ou1[0][I1] = u0;
+                ou1[1][I1] = u1;
+                oacc[0][I1] = k0;
+                oacc[1][I1] = k1;
+                S[ubuf(1, P1) + c.oe] = u0;
+                S[ubuf(1, P1) + c.oe + kHeatHalf] = u1;
+                if (ZEdge && p == 0) {  // insulated bottom face: u1(-1) := u1(0)
+                    ou1[0][I2] = u0;
+                    ou1[1][I2] = u1;
                 }
-                block_eval(ctr, zm, zp, lvl(0, P1), kv);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    u[k] = Exact ? ctr[k] + sc.h2 * kv[k] : fma(hp.h2kk, kv[k], ctr[k]);
-                    ou1[k][I1] = u[k];
-                    oacc[k][I1] = kv[k];
-                }
-                block_store(lvl(1, P1), u);
                 if (c.rd[0] >= 1) {
-                    const double s = r0x[I1];
-                    const double kr = ring_eval(c.ro[0], c.rf[0], s, hm ? r0x[I2] : s, hpz ? r0pre[P0] : s, lvl(0, P1));
-                    const double uu = Exact ? s + sc.h2 * kr : fma(hp.h2kk, kr, s);
-                    r0u1[I1] = uu;
-                    S[lvl(1, P1) + c.ro[0]] = uu;
+                    const double s = rx[I1];
+                    const double kr = ring_eval(s, rx[I2], rxj, X1);
+                    const double uu = upd(s, kr, sc.h2, hp.h2kk);
+                    ru1[I1] = uu;
+                    S[ubuf(1, P1) + c.ro[0]] = uu;
+                    if (ZEdge && p == 0) ru1[I2] = uu;
                 }
-                if (c.rd[1] >= 1) {
-                    const double s = r1x[I1];
-                    const double kr = ring_eval(c.ro[1], c.rf[1], s, hm ? r1x[I2] : s, hpz ? r1pre[P0] : s, lvl(0, P1));
-                    const double uu = Exact ? s + sc.h2 * kr : fma(hp.h2kk, kr, s);
-                    r1u1[I1] = uu;
-                    S[lvl(1, P1) + c.ro[1]] = uu;
-                }
+            } else if (ZEdge && p == g) {  // top face: u1(g) := u1(g-1)
+                ou1[0][I1] = ou1[0][I2];
+                ou1[1][I1] = ou1[1][I2];
+                ru1[I1] = ru1[I2];
             }
         }
         // ---------------- stage 2 at plane p = j-2
         {
             const int p = j - 2;
             if (p >= zs + 2 * lo_shift && p < ze - 2 * hi_shift) {
-                const bool hm = p > 0, hpz = p + 1 < g;
-                double ctr[4], zm[4], zp[4], kv[4], u[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    ctr[k] = ou1[k][I2];
-                    zm[k] = hm ? ou1[k][I3] : ctr[k];
-                    zp[k] = hpz ? ou1[k][I1] : ctr[k];
+                double k0, k1;
+                pair_eval(ou1[0][I2], ou1[1][I2], ou1[0][I3], ou1[1][I3], ou1[0][I1], ou1[1][I1],
+                          ubuf(1, P0), k0, k1);
+                const double u0 = upd(ox[0][I2], k0, sc.h2, hp.h2kk);
+                const double u1 = upd(ox[1][I2], k1, sc.h2, hp.h2kk);
+                ou2[0][I2] = u0;
+                ou2[1][I2] = u1;
+                oacc[0][I2] = fma(2.0, k0, oacc[0][I2]);  // acc + 2k (exact: 2k is exact)
+                oacc[1][I2] = fma(2.0, k1, oacc[1][I2]);
+                S[ubuf(2, P0) + c.oe] = u0;
+                S[ubuf(2, P0) + c.oe + kHeatHalf] = u1;
+                if (ZEdge && p == 0) {
+                    ou2[0][I3] = u0;
+                    ou2[1][I3] = u1;
                 }
-                block_eval(ctr, zm, zp, lvl(1, P0), kv);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const double x = ox[k][I2];
-                    u[k] = Exact ? x + sc.h2 * kv[k] : fma(hp.h2kk, kv[k], x);
-                    ou2[k][I2] = u[k];
-                    oacc[k][I2] = fma(2.0, kv[k], oacc[k][I2]);  // acc + 2k (exact: 2k is exact)
-                }
-                block_store(lvl(2, P0), u);
                 if (c.rd[0] >= 2) {
-                    const double s = r0u1[I2];
-                    const double kr = ring_eval(c.ro[0], c.rf[0], s, hm ? r0u1[I3] : s, hpz ? r0u1[I1] : s, lvl(1, P0));
-                    const double x = r0x[I2];
-                    const double uu = Exact ? x + sc.h2 * kr : fma(hp.h2kk, kr, x);
-                    r0u2[I2] = uu;
-                    S[lvl(2, P0) + c.ro[0]] = uu;
+                    const double s = ru1[I2];
+                    const double kr = ring_eval(s, ru1[I3], ru1[I1], ubuf(1, P0));
+                    const double uu = upd(rx[I2], kr, sc.h2, hp.h2kk);
+                    ru2[I2] = uu;
+                    S[ubuf(2, P0) + c.ro[0]] = uu;
+                    if (ZEdge && p == 0) ru2[I3] = uu;
                 }
-                if (c.rd[1] >= 2) {
-                    const double s = r1u1[I2];
-                    const double kr = ring_eval(c.ro[1], c.rf[1], s, hm ? r1u1[I3] : s, hpz ? r1u1[I1] : s, lvl(1, P0));
-                    const double x = r1x[I2];
-                    const double uu = Exact ? x + sc.h2 * kr : fma(hp.h2kk, kr, x);
-                    S[lvl(2, P0) + c.ro[1]] = uu;
-                }
+            } else if (ZEdge && p == g) {
+                ou2[0][I2] = ou2[0][I3];
+                ou2[1][I2] = ou2[1][I3];
+                ru2[I2] = ru2[I3];
             }
         }
         // ---------------- stage 3 at plane p = j-3
         {
             const int p = j - 3;
             if (p >= zs + 3 * lo_shift && p < ze - 3 * hi_shift) {
-                const bool hm = p > 0, hpz = p + 1 < g;
-                double ctr[4], zm[4], zp[4], kv[4], u[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    ctr[k] = ou2[k][I3];
-                    zm[k] = hm ? ou2[k][I0] : ctr[k];   // plane j-4 shares slot I0
-                    zp[k] = hpz ? ou2[k][I2] : ctr[k];
+                double k0, k1;
+                pair_eval(ou2[0][I3], ou2[1][I3], ou2[0][I0], ou2[1][I0], ou2[0][I2], ou2[1][I2],
+                          ubuf(2, P1), k0, k1);
+                // x(j-3) from the shared x ring (keeps the register budget at 128)
+                const double u0 = upd(S[X3 + c.oe], k0, sc.hk, hp.hkk);
+                const double u1 = upd(S[X3 + c.oe + kHeatHalf], k1, sc.hk, hp.hkk);
+                ou3[0][I3] = u0;
+                ou3[1][I3] = u1;
+                oacc[0][I3] = fma(2.0, k0, oacc[0][I3]);
+                oacc[1][I3] = fma(2.0, k1, oacc[1][I3]);
+                S[ubuf(3, P1) + c.oe] = u0;
+                S[ubuf(3, P1) + c.oe + kHeatHalf] = u1;
+                if (ZEdge && p == 0) {
+                    ou3[0][I0] = u0;
+                    ou3[1][I0] = u1;
                 }
-                block_eval(ctr, zm, zp, lvl(2, P1), kv);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const double x = ox[k][I3];
-                    u[k] = Exact ? x + sc.hk * kv[k] : fma(hp.hkk, kv[k], x);
-                    ou3[k][I3] = u[k];
-                    oacc[k][I3] = fma(2.0, kv[k], oacc[k][I3]);
-                }
-                block_store(lvl(3, P1), u);
                 if (c.rd[0] >= 3) {
-                    const double s = r0u2[I3];
-                    const double kr = ring_eval(c.ro[0], c.rf[0], s, hm ? r0u2[I0] : s, hpz ? r0u2[I2] : s, lvl(2, P1));
-                    const double x = r0x[I3];
-                    const double uu = Exact ? x + sc.hk * kr : fma(hp.hkk, kr, x);
-                    S[lvl(3, P1) + c.ro[0]] = uu;
+                    const double s = ru2[I3];
+                    const double kr = ring_eval(s, ru2[I0], ru2[I2], ubuf(2, P1));
+                    S[ubuf(3, P1) + c.ro[0]] = upd(S[X3 + c.ro[0]], kr, sc.hk, hp.hkk);
                 }
+            } else if (ZEdge && p == g) {
+                ou3[0][I3] = ou3[0][I0];
+                ou3[1][I3] = ou3[1][I0];
             }
         }
-        // ---------------- stage 4 at plane p = j-4 (own block), stored to HBM
+        // ---------------- stage 4 at plane p = j-4 (own pair), stored to HBM
         {
             const int p = j - 4;
             if (p >= ob && p < oe) {
-                const bool hm = p > 0, hpz = p + 1 < g;
-                double ctr[4], zm[4], zp[4], kv[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    ctr[k] = ou3[k][I0];
-                    zm[k] = hm ? ou3[k][I1] : ctr[k];   // plane j-5 shares slot I1
-                    zp[k] = hpz ? ou3[k][I3] : ctr[k];
-                }
-                block_eval(ctr, zm, zp, lvl(3, P0), kv);
+                double k0, k1;
+                pair_eval(ou3[0][I0], ou3[1][I0], ou3[0][I1], ou3[1][I1], ou3[0][I3], ou3[1][I3],
+                          ubuf(3, P0), k0, k1);
                 double* out = dst + static_cast<long long>(p) * g2;
+                const double kk[2] = {k0, k1};
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < 2; ++k) {
                     if (!in(k)) continue;
-                    const double x = ox[k][I0];
-                    const double xn = Exact ? x + sc.h6 * (oacc[k][I0] + kv[k])
-                                            : fma(hp.h6kk, oacc[k][I0] + kv[k], x);
-                    out[c.og[k]] = xn;
+                    const double x = S[X4 + c.oe + k * kHeatHalf];  // x(j-4)
+                    const double xn = Exact ? x + sc.h6 * (oacc[k][I0] + kk[k])
+                                            : fma(hp.h6kk, oacc[k][I0] + kk[k], x);
+                    out[c.og + k] = xn;
                     if (!finite_d(xn)) {
                         const unsigned long long gi = static_cast<unsigned long long>(
-                            static_cast<long long>(p) * g2 + c.og[k]);
+                            static_cast<long long>(p) * g2 + c.og + k);
                         if (method == 0)
                             record_fail(fail, step, gi + (field ? n_total : 0ull));
                         else if (fail)
@@ -328,23 +332,51 @@ struct HeatRun {
                 }
             }
         }
-        // x(j) moves from the prefetch register into the history slot of x(j-4)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) ox[k][I0] = opre[k][P0];
-        r0x[I0] = r0pre[P0];
-        r1x[I0] = r1pre[P0];
+        // x(j) joins the history in the slot of x(j-4)
+        ox[0][I0] = xj0;
+        ox[1][I0] = xj1;
+        rx[I0] = rxj;
+        if (ZEdge && j == 0) {  // insulated bottom face: x(-1) := x(0)
+            ox[0][I1] = xj0;
+            ox[1][I1] = xj1;
+            rx[I1] = rxj;
+        }
+        cp_async_wait_all();  // x(j+1) landed (own copies); barrier publishes it
         __syncthreads();
     }
 
-    __device__ __forceinline__ void run() {
-        if (zs < ze) load(zs, 0);
-        const int jend = ze + kHeatH;
-        for (int j = zs; j < jend; j += 4) {
-            iteration<0>(j);
-            if (j + 1 < jend) iteration<1>(j + 1);
-            if (j + 2 < jend) iteration<2>(j + 2);
-            if (j + 3 < jend) iteration<3>(j + 3);
+    template <bool ZEdge>
+    __device__ __forceinline__ void one(int j) {
+        switch ((j - zs) & 3) {
+            case 0: iteration<0, ZEdge>(j); break;
+            case 1: iteration<1, ZEdge>(j); break;
+            case 2: iteration<2, ZEdge>(j); break;
+            default: iteration<3, ZEdge>(j); break;
         }
+    }
+
+    __device__ __forceinline__ void run() {
+        if (zs < ze) {
+            load(zs, 0);
+            cp_async_wait_all();
+        }
+        __syncthreads();
+        const int jend = ze + kHeatH;
+        // iterations whose planes j-5 .. j touch no insulated z face: 5 <= j < g
+        int a = (zs > 5) ? zs : 5;
+        a = zs + ((a - zs + 3) & ~3);          // keep (j - zs) % 4 == 0 at the main loop start
+        int b = (jend < g) ? jend : g;
+        if (b < a) b = a;
+        const int main_end = a + ((b - a) & ~3);
+        int j = zs;
+        for (; j < a && j < jend; ++j) one<true>(j);
+        for (; j < main_end; j += 4) {
+            iteration<0, false>(j);
+            iteration<1, false>(j + 1);
+            iteration<2, false>(j + 2);
+            iteration<3, false>(j + 3);
+        }
+        for (; j < jend; ++j) one<true>(j);
     }
 };
 
@@ -369,18 +401,17 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
     // ---- static column assignment
     HeatCols c;
     {
-        const int bx = tid & 15, by = tid >> 4;
-        c.ob = (2 * by + kHeatH) * kHeatP + (2 * bx + kHeatH);
+        const int bx = tid & 15, by = tid >> 4;           // own pair (2bx, by) in tile coords
+        c.oe = heat_sidx(2 * bx + kHeatH, by + kHeatH);
+        const long long ix = ix0 + 2 * bx, iy = iy0 + by;
+        c.of[0] = face_flags(ix, iy, g);
+        c.of[1] = face_flags(ix + 1, iy, g);
+        c.og = (c.of[0] & kIn) ? static_cast<int>(iy * g + ix) : 0;
+        // halo-ring columns ordered by distance d = 1..4 from the tile (a column
+        // at distance d is computed at stages 1 .. 4-d); slot 0: ring index tid,
+        // slot 1: ring index 512 + tid (distance 4, load only)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const long long ix = ix0 + 2 * bx + (k & 1), iy = iy0 + 2 * by + (k >> 1);
-            c.of[k] = face_flags(ix, iy, g);
-            c.og[k] = (c.of[k] & kIn) ? static_cast<int>(iy * g + ix) : 0;
-        }
-        // halo-ring columns ordered by distance d = 1..4 from the tile
-        // (a column at distance d is computed at stages 1 .. 4-d)
-#pragma unroll
-        for (int s = 0; s < kHeatRingSlots; ++s) {
+        for (int s = 0; s < 2; ++s) {
             int r = tid + s * kHeatThreads;
             c.ro[s] = 0;
             c.rg[s] = 0;
@@ -389,17 +420,17 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
             for (int d = 1; d <= kHeatH; ++d) {
                 const int side = kHeatT + 2 * d, cnt = 4 * side - 4;
                 if (r < cnt) {
-                    const int lo = kHeatH - d;  // region coordinate of the band's first row/col
+                    const int lo = kHeatH - d;  // footprint coordinate of the band's first row/col
                     int x, y;
                     if (r < side) { y = lo; x = lo + r; }
                     else if (r < 2 * side) { y = lo + side - 1; x = lo + (r - side); }
                     else if (r < 3 * side - 2) { x = lo; y = lo + 1 + (r - 2 * side); }
                     else { x = lo + side - 1; y = lo + 1 + (r - (3 * side - 2)); }
-                    const long long ix = ix0 - kHeatH + x, iy = iy0 - kHeatH + y;
-                    c.ro[s] = y * kHeatP + x;
-                    c.rf[s] = face_flags(ix, iy, g);
+                    const long long gx = ix0 - kHeatH + x, gy = iy0 - kHeatH + y;
+                    c.ro[s] = heat_sidx(x, y);
+                    c.rf[s] = face_flags(gx, gy, g) | ((x & 1) ? kOdd : 0);
                     if (c.rf[s] & kIn) {
-                        c.rg[s] = static_cast<int>(iy * g + ix);
+                        c.rg[s] = static_cast<int>(gy * g + gx);
                         c.rd[s] = kHeatH - d;
                     }
                     break;
