@@ -45,9 +45,11 @@ public:
     pirk_ctx* get() const { return ctx_; }
     void set_mode(pirk_mode m) { pirk_set_mode(ctx_, m); }
 
+    // Process-wide default device.  Intentionally never destroyed: releasing
+    // CUDA resources from a static destructor can race the CUDA runtime's own
+    // teardown at exit.
     static Device& current() {
-        thread_local std::unique_ptr<Device> dev;
-        if (!dev) dev = std::make_unique<Device>(0);
+        static Device* dev = new Device(0);
         return *dev;
     }
 

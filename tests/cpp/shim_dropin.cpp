@@ -13,6 +13,7 @@ using namespace ivreach;
 static int failures = 0;
 static void check(bool ok, const char* what) {
     std::printf("%s: %s\n", ok ? "ok" : "FAIL", what);
+    std::fflush(stdout);
     if (!ok) ++failures;
 }
 
@@ -20,7 +21,8 @@ int main() {
     const double kE = 2.718281828459045;
     {   // test_reach.cpp:70-75
         ReachProblem p{make_scalar_linear(), IntervalVector({1.0}, {2.0}), std::nullopt, 0.0, 1.0, 0.001, 0};
-        const IntervalVector& fin = mixed_monotonicity(p, 1).entries.back().box;
+        const ReachTube tube = mixed_monotonicity(p, 1);
+        const IntervalVector& fin = tube.entries.back().box;
         check(std::fabs(fin.lower(0) - kE) <= 1e-4 && std::fabs(fin.upper(0) - 2 * kE) <= 1e-4,
               "mixed monotonicity exact on xdot = x");
     }
