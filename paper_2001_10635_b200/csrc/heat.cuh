@@ -155,8 +155,11 @@ struct HeatRun {
     __device__ __forceinline__ bool in(int k) const { return Interior || (c.of[k] & kIn); }
 
     // x(p) of this thread's columns: global -> shared x-ring slot s (async)
-    __device__ __forceinline__ void load(int p, int s) {
-        const double* plane = src + static_cast<long long>(p) * g2;
+    // running plane pointers: x-plane j+1 (loads) and output plane j-4 (stores)
+    const double* ldp;
+    double* stp;
+
+    __device__ __forceinline__ void load(const double* plane, int s) {
         double* X = S + xbuf(s);
         if (in(0)) cp_async8(X + c.oe, plane + c.og);
         if (in(1)) cp_async8(X + c.oe + kHeatHalf, plane + c.og + 1);
@@ -200,7 +203,7 @@ struct HeatRun {
         const int x8 = (j - zs) & 7;                   // x-ring slot of plane j
         const int X0 = xbuf(x8), X1 = xbuf((x8 + 7) & 7), X3 = xbuf((x8 + 5) & 7),
                   X4 = xbuf((x8 + 4) & 7);
-        if (j + 1 < ze) load(j + 1, (x8 + 1) & 7);  // slot of x(j-7): no longer read
+        if (j + 1 < ze) load(ldp, (x8 + 1) & 7);  // x(j+1) into the slot of x(j-7)
         // own x(j) (arrived last iteration): the z+ neighbour of stage 1
         double xj0 = S[X0 + c.oe], xj1 = S[X0 + c.oe + kHeatHalf];
         double rxj = S[X0 + c.ro[0]];
@@ -213,7 +216,7 @@ struct HeatRun {
         // ---------------- stage 1 at plane p = j-1
         {
             const int p = j - 1;
-            if (p >= zs + lo_shift && p < ze - hi_shift) {
+            if (!ZEdge || (p >= zs + lo_shift && p < ze - hi_shift)) {
                 double k0, k1;
                 pair_eval(ox[0][I1], ox[1][I1], ox[0][I2], ox[1][I2], xj0, xj1, X1, k0, k1);
                 const double u0 = upd(ox[0][I1], k0, sc.h2, hp.h2kk);
@@ -245,7 +248,7 @@ struct HeatRun {
         // ---------------- stage 2 at plane p = j-2
         {
             const int p = j - 2;
-            if (p >= zs + 2 * lo_shift && p < ze - 2 * hi_shift) {
+            if (!ZEdge || (p >= zs + 2 * lo_shift && p < ze - 2 * hi_shift)) {
                 double k0, k1;
                 pair_eval(ou1[0][I2], ou1[1][I2], ou1[0][I3], ou1[1][I3], ou1[0][I1], ou1[1][I1],
                           ubuf(1, P0), k0, k1);
@@ -278,7 +281,7 @@ struct HeatRun {
         // ---------------- stage 3 at plane p = j-3
         {
             const int p = j - 3;
-            if (p >= zs + 3 * lo_shift && p < ze - 3 * hi_shift) {
+            if (!ZEdge || (p >= zs + 3 * lo_shift && p < ze - 3 * hi_shift)) {
                 double k0, k1;
                 pair_eval(ou2[0][I3], ou2[1][I3], ou2[0][I0], ou2[1][I0], ou2[0][I2], ou2[1][I2],
                           ubuf(2, P1), k0, k1);
@@ -308,11 +311,11 @@ struct HeatRun {
         // ---------------- stage 4 at plane p = j-4 (own pair), stored to HBM
         {
             const int p = j - 4;
-            if (p >= ob && p < oe) {
+            if (!ZEdge || (p >= ob && p < oe)) {
                 double k0, k1;
                 pair_eval(ou3[0][I0], ou3[1][I0], ou3[0][I1], ou3[1][I1], ou3[0][I3], ou3[1][I3],
                           ubuf(3, P0), k0, k1);
-                double* out = dst + static_cast<long long>(p) * g2;
+                double* out = stp;
                 const double kk[2] = {k0, k1};
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
@@ -341,6 +344,8 @@ struct HeatRun {
             ox[1][I1] = xj1;
             rx[I1] = rxj;
         }
+        ldp += g2;
+        stp += g2;
         cp_async_wait_all();  // x(j+1) landed (own copies); barrier publishes it
         __syncthreads();
     }
@@ -357,15 +362,23 @@ struct HeatRun {
 
     __device__ __forceinline__ void run() {
         if (zs < ze) {
-            load(zs, 0);
+            load(src + static_cast<long long>(zs) * g2, 0);
             cp_async_wait_all();
         }
         __syncthreads();
+        ldp = src + static_cast<long long>(zs + 1) * g2;
+        stp = dst + static_cast<long long>(zs - 4) * g2;
         const int jend = ze + kHeatH;
-        // iterations whose planes j-5 .. j touch no insulated z face: 5 <= j < g
-        int a = (zs > 5) ? zs : 5;
+        // Steady-state iterations: all four stages valid and planes j-5 .. j
+        // clear of the insulated z faces, so the unrolled main loop carries no
+        // validity or boundary branches.
+        int a = zs + 3 + 3 * lo_shift;
+        if (a < ob + 4) a = ob + 4;
+        if (a < 5) a = 5;
         a = zs + ((a - zs + 3) & ~3);          // keep (j - zs) % 4 == 0 at the main loop start
-        int b = (jend < g) ? jend : g;
+        int b = ze + 1 - hi_shift;
+        if (b > oe + 4) b = oe + 4;
+        if (b > g) b = g;
         if (b < a) b = a;
         const int main_end = a + ((b - a) & ~3);
         int j = zs;
