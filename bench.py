@@ -331,6 +331,16 @@ def run_ours(args):
                      "avg_launch_ms": per_launch_ms},
         "finite": ok,
     }
+    if args.mode == "fast" and not args.no_exact:
+        # the bit-exact arithmetic mode on the same workload (reported beside the headline)
+        import copy
+
+        a2 = copy.copy(args)
+        a2.mode = "exact"
+        ms_e, _, clk_e, _, _ = heat_device_bench(a2, world, rank, local, torch, pk, dist)
+        line["exact_mode"] = {"value": updates / (ms_e * 1e-3), "ms_per_step": ms_e / args.steps,
+                              "roofline_frac": (launch_bytes / (ms_e / args.steps * 1e-3) / 1e9) / hbm,
+                              "clocks": clk_e}
     if rank == 0 and not args.no_e2e and world == 1:
         e2e, ok2 = heat_e2e(args, pk, torch, world)
         line["e2e"] = e2e
@@ -403,6 +413,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-exact", action="store_true")
     ap.add_argument("--check", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
