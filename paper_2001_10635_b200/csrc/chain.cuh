@@ -39,8 +39,25 @@ __device__ __forceinline__ double traffic_flux(const ChainModel& m, double from,
     }
 }
 
-// s(z) = z / (1 + |z|) for the coupled chain.
-__device__ __forceinline__ double chain_sat(double z) { return z / (1.0 + fabs(z)); }
+// s(z) = z / (1 + |z|) for the coupled chain.  Exact mode: IEEE division.
+// Fast mode: the denominator lies in [1, inf), so a hardware reciprocal
+// estimate refined by two Newton steps (~1 ulp) replaces the full division
+// and its special-case branches.
+template <bool Exact>
+__device__ __forceinline__ double chain_sat(double z) {
+    const double d = 1.0 + fabs(z);
+    if constexpr (Exact) {
+        return z / d;
+    } else {
+        double r;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+        double e = fma(-d, r, 1.0);
+        r = fma(r, e, r);
+        e = fma(-d, r, 1.0);
+        r = fma(r, e, r);
+        return z * r;
+    }
+}
 
 template <bool Exact, int Kind, int Method>
 __global__ void __launch_bounds__(kChainThreads)
@@ -101,8 +118,8 @@ chain_step_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc,
             for (int r = 0; r < kChainPerThread; ++r) {
                 const int j = tid + r * kChainThreads;
                 if (j >= s && j < kChainSpan - s) {
-                    sA[0][j] = chain_sat(u0[j]);
-                    sA[1][j] = chain_sat(u1[j]);
+                    sA[0][j] = chain_sat<Exact>(u0[j]);
+                    sA[1][j] = chain_sat<Exact>(u1[j]);
                 }
             }
             __syncthreads();
