@@ -38,6 +38,10 @@
 // constants folded with k.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (encoded through cudaGetDriverEntryPoint)
+
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -50,9 +54,11 @@ constexpr int kHeatHalf = kHeatW / 2;        // 20: even / odd column sub-rows
 constexpr int kHeatP = kHeatW + 1;           // 41: odd row pitch (bank-conflict free)
 constexpr int kHeatPlane = kHeatW * kHeatP;  // 1640
 constexpr int kHeatThreads = 512;            // one 1x2 own pair per thread
-constexpr int kHeatXRing = 8;                // x planes j-4 .. j+1 (slot (p - zs) & 7)
-constexpr int kHeatPlanes = kHeatXRing + 3 * 2;  // + u1/u2/u3 double buffers
-constexpr size_t kHeatSmemBytes = size_t(kHeatPlanes) * kHeatPlane * sizeof(double);  // 183,680 B
+constexpr int kHeatXRing = 8;                // x planes j-7 .. j (slot (p - zs) & 7)
+// x planes are row-major 40x40 (the TMA box), each slot padded to a 128-byte multiple
+constexpr int kHeatXSlot = 1664;             // >= 1600 doubles, 13,312 B
+constexpr size_t kHeatSmemBytes =
+    size_t(kHeatXRing) * kHeatXSlot * sizeof(double) + size_t(6) * kHeatPlane * sizeof(double);  // 185,216 B
 
 struct HeatStepParams {
     double kk, robin;
@@ -77,18 +83,48 @@ __device__ __forceinline__ int heat_sidx(int x, int y) {
     return y * kHeatP + (x & 1) * kHeatHalf + (x >> 1);
 }
 
-// buffer bases: x ring slot s (0..7); level L (1..3) parity par
-__device__ __forceinline__ constexpr int xbuf(int s) { return s * kHeatPlane; }
+// buffer bases: x ring slot s (0..7, row-major); level L (1..3) parity par (de-interleaved)
+__device__ __forceinline__ constexpr int xbuf(int s) { return s * kHeatXSlot; }
 __device__ __forceinline__ constexpr int ubuf(int L, int par) {
-    return (kHeatXRing + 2 * (L - 1) + par) * kHeatPlane;
+    return kHeatXRing * kHeatXSlot + (2 * (L - 1) + par) * kHeatPlane;
 }
 
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// TMA: one 40x40 x-plane box per iteration, completing on an mbarrier.
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\nPIRK_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra PIRK_WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_plane(double* dst, const void* tmap, int x, int y, int z,
+                                               unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+        "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
 
 // Stencil value from the six neighbours.  Exact: k = kk*acc.  Fast: t = sum - 6 s.
 template <bool Exact, bool Interior>
@@ -124,6 +160,8 @@ __device__ __forceinline__ double heat_pt(double s, double xm, double xp, double
 }
 
 struct HeatCols {
+    int xe;        // row-major x-ring index of the pair's even column (odd: xe + 1)
+    int xr[2];     // row-major x-ring index of the halo-ring columns
     int oe;        // shared index of the pair's even column (the odd one is oe + 20)
     int og;        // in-plane global offset of the even column (odd: og + 1)
     int of[2];     // face flags of the two own columns
@@ -133,7 +171,7 @@ struct HeatCols {
     int rd[2];     // number of stages computed at the column (0..3; -1: none)
 };
 
-template <bool Exact, bool Interior>
+template <bool Exact, bool Interior, bool Tma>
 struct HeatRun {
     const HeatStepParams& hp;
     const StepConsts& sc;
@@ -147,6 +185,10 @@ struct HeatRun {
     unsigned long long step;
     unsigned long long* fail;
     unsigned long long n_total;
+    // TMA: tensor map of this field's window, box origin (x, y), window start plane, barriers
+    const void* tmap;
+    int bx0, by0, wbz;
+    unsigned long long* bars;
 
     // register state: slot (p - zs) & 3 of plane p
     double ox[2][4], ou1[2][4], ou2[2][4], ou3[2][4], oacc[2][4];
@@ -154,18 +196,44 @@ struct HeatRun {
 
     __device__ __forceinline__ bool in(int k) const { return Interior || (c.of[k] & kIn); }
 
-    // x(p) of this thread's columns: global -> shared x-ring slot s (async)
     // running plane pointers: x-plane j+1 (loads) and output plane j-4 (stores)
     const double* ldp;
     double* stp;
 
-    __device__ __forceinline__ void load(const double* plane, int s) {
+    // x-plane p -> x-ring slot s.  TMA: one thread issues the whole 40x40 box
+    // (out-of-grid cells zero-filled), completion on bars[s].  Fallback: each
+    // thread cp.asyncs its own columns (completed by cp_async_wait_all).
+    __device__ __forceinline__ void load(const double* plane, int p, int s) {
         double* X = S + xbuf(s);
-        if (in(0)) cp_async8(X + c.oe, plane + c.og);
-        if (in(1)) cp_async8(X + c.oe + kHeatHalf, plane + c.og + 1);
-        if (c.rd[0] >= 0) cp_async8(X + c.ro[0], plane + c.rg[0]);
-        if (c.rd[1] >= 0) cp_async8(X + c.ro[1], plane + c.rg[1]);
-        cp_async_commit();
+        if constexpr (Tma) {
+            if (threadIdx.x == 0) {
+                mbar_expect_tx(bars + s, kHeatW * kHeatW * sizeof(double));
+                tma_load_plane(X, tmap, bx0, by0, p - wbz, bars + s);
+            }
+        } else {
+            if (in(0)) cp_async8(X + c.xe, plane + c.og);
+            if (in(1)) cp_async8(X + c.xe + 1, plane + c.og + 1);
+            if (c.rd[0] >= 0) cp_async8(X + c.xr[0], plane + c.rg[0]);
+            if (c.rd[1] >= 0) cp_async8(X + c.xr[1], plane + c.rg[1]);
+            cp_async_commit();
+        }
+    }
+
+    // stage 1 reads the row-major x plane
+    __device__ __forceinline__ void pair_eval_x(double c0, double c1, double zm0, double zm1,
+                                                double zp0, double zp1, int x_off, double& k0,
+                                                double& k1) const {
+        const double* B = S + x_off + c.xe;
+        const double l = B[-1], r = B[2];
+        const double u0 = B[-kHeatW], u1 = B[1 - kHeatW];
+        const double d0 = B[kHeatW], d1 = B[kHeatW + 1];
+        k0 = heat_pt<Exact, Interior>(c0, l, c1, u0, d0, zm0, zp0, c.of[0], hp);
+        k1 = heat_pt<Exact, Interior>(c1, c0, r, u1, d1, zm1, zp1, c.of[1], hp);
+    }
+
+    __device__ __forceinline__ double ring_eval_x(double s, double zm, double zp, int x_off) const {
+        const double* B = S + x_off + c.xr[0];
+        return heat_pt<Exact, Interior>(s, B[-1], B[1], B[-kHeatW], B[kHeatW], zm, zp, c.rf[0], hp);
     }
 
     // own pair: centres c0 (even col) and c1 (odd col) at level L-1 of plane p,
@@ -203,10 +271,13 @@ struct HeatRun {
         const int x8 = (j - zs) & 7;                   // x-ring slot of plane j
         const int X0 = xbuf(x8), X1 = xbuf((x8 + 7) & 7), X3 = xbuf((x8 + 5) & 7),
                   X4 = xbuf((x8 + 4) & 7);
-        if (j + 1 < ze) load(ldp, (x8 + 1) & 7);  // x(j+1) into the slot of x(j-7)
-        // own x(j) (arrived last iteration): the z+ neighbour of stage 1
-        double xj0 = S[X0 + c.oe], xj1 = S[X0 + c.oe + kHeatHalf];
-        double rxj = S[X0 + c.ro[0]];
+        if constexpr (Tma) {
+            if (j < ze) mbar_wait(bars + x8, ((j - zs) >> 3) & 1);  // x(j) landed
+        }
+        if (j + 1 < ze) load(ldp, j + 1, (x8 + 1) & 7);  // x(j+1) into the slot of x(j-7)
+        // own x(j): the z+ neighbour of stage 1
+        double xj0 = S[X0 + c.xe], xj1 = S[X0 + c.xe + 1];
+        double rxj = S[X0 + c.xr[0]];
         if (ZEdge && j == g) {  // insulated top face: x(g) := x(g-1)
             xj0 = ox[0][I1];
             xj1 = ox[1][I1];
@@ -218,7 +289,7 @@ struct HeatRun {
             const int p = j - 1;
             if (!ZEdge || (p >= zs + lo_shift && p < ze - hi_shift)) {
                 double k0, k1;
-                pair_eval(ox[0][I1], ox[1][I1], ox[0][I2], ox[1][I2], xj0, xj1, X1, k0, k1);
+                pair_eval_x(ox[0][I1], ox[1][I1], ox[0][I2], ox[1][I2], xj0, xj1, X1, k0, k1);
                 const double u0 = upd(ox[0][I1], k0, sc.h2, hp.h2kk);
                 const double u1 = upd(ox[1][I1], k1, sc.h2, hp.h2kk);
                 ou1[0][I1] = u0;
@@ -233,7 +304,7 @@ struct HeatRun {
                 }
                 if (c.rd[0] >= 1) {
                     const double s = rx[I1];
-                    const double kr = ring_eval(s, rx[I2], rxj, X1);
+                    const double kr = ring_eval_x(s, rx[I2], rxj, X1);
                     const double uu = upd(s, kr, sc.h2, hp.h2kk);
                     ru1[I1] = uu;
                     S[ubuf(1, P1) + c.ro[0]] = uu;
@@ -286,8 +357,8 @@ struct HeatRun {
                 pair_eval(ou2[0][I3], ou2[1][I3], ou2[0][I0], ou2[1][I0], ou2[0][I2], ou2[1][I2],
                           ubuf(2, P1), k0, k1);
                 // x(j-3) from the shared x ring (keeps the register budget at 128)
-                const double u0 = upd(S[X3 + c.oe], k0, sc.hk, hp.hkk);
-                const double u1 = upd(S[X3 + c.oe + kHeatHalf], k1, sc.hk, hp.hkk);
+                const double u0 = upd(S[X3 + c.xe], k0, sc.hk, hp.hkk);
+                const double u1 = upd(S[X3 + c.xe + 1], k1, sc.hk, hp.hkk);
                 ou3[0][I3] = u0;
                 ou3[1][I3] = u1;
                 oacc[0][I3] = fma(2.0, k0, oacc[0][I3]);
@@ -301,7 +372,7 @@ struct HeatRun {
                 if (c.rd[0] >= 3) {
                     const double s = ru2[I3];
                     const double kr = ring_eval(s, ru2[I0], ru2[I2], ubuf(2, P1));
-                    S[ubuf(3, P1) + c.ro[0]] = upd(S[X3 + c.ro[0]], kr, sc.hk, hp.hkk);
+                    S[ubuf(3, P1) + c.ro[0]] = upd(S[X3 + c.xr[0]], kr, sc.hk, hp.hkk);
                 }
             } else if (ZEdge && p == g) {
                 ou3[0][I3] = ou3[0][I0];
@@ -320,7 +391,7 @@ struct HeatRun {
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
                     if (!in(k)) continue;
-                    const double x = S[X4 + c.oe + k * kHeatHalf];  // x(j-4)
+                    const double x = S[X4 + c.xe + k];  // x(j-4)
                     const double xn = Exact ? x + sc.h6 * (oacc[k][I0] + kk[k])
                                             : fma(hp.h6kk, oacc[k][I0] + kk[k], x);
                     out[c.og + k] = xn;
@@ -346,7 +417,7 @@ struct HeatRun {
         }
         ldp += g2;
         stp += g2;
-        cp_async_wait_all();  // x(j+1) landed (own copies); barrier publishes it
+        if constexpr (!Tma) cp_async_wait_all();  // x(j+1) landed (own copies); barrier publishes it
         __syncthreads();
     }
 
@@ -362,8 +433,8 @@ struct HeatRun {
 
     __device__ __forceinline__ void run() {
         if (zs < ze) {
-            load(src + static_cast<long long>(zs) * g2, 0);
-            cp_async_wait_all();
+            load(src + static_cast<long long>(zs) * g2, zs, 0);  // x(zs) -> slot 0
+            if constexpr (!Tma) cp_async_wait_all();
         }
         __syncthreads();
         ldp = src + static_cast<long long>(zs + 1) * g2;
@@ -393,13 +464,21 @@ struct HeatRun {
     }
 };
 
+// Tensor maps of the two fields' windows (used when `tma` is set): a
+// 3-D (x, y, plane) fp64 view with a 40x40x1 box.
+struct HeatTmaps {
+    CUtensorMap f[2];
+};
+
 template <bool Exact>
 __global__ void __launch_bounds__(kHeatThreads, 1)
 heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
                  const StepConsts sc, const unsigned long long step, const uint64_t zchunk,
-                 unsigned long long* __restrict__ fail) {
+                 unsigned long long* __restrict__ fail, const __grid_constant__ HeatTmaps tm,
+                 const int tma) {
     (void)sizeof(ModeCheck<Exact>);
-    extern __shared__ __align__(16) double smem[];
+    extern __shared__ __align__(128) double smem[];
+    __shared__ __align__(8) unsigned long long bars[kHeatXRing];
     const int tid = threadIdx.x;
     const long long g = static_cast<long long>(m.g);
     const int field = blockIdx.z & 1;
@@ -416,6 +495,7 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
     {
         const int bx = tid & 15, by = tid >> 4;           // own pair (2bx, by) in tile coords
         c.oe = heat_sidx(2 * bx + kHeatH, by + kHeatH);
+        c.xe = (by + kHeatH) * kHeatW + (2 * bx + kHeatH);
         const long long ix = ix0 + 2 * bx, iy = iy0 + by;
         c.of[0] = face_flags(ix, iy, g);
         c.of[1] = face_flags(ix + 1, iy, g);
@@ -427,6 +507,7 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
         for (int s = 0; s < 2; ++s) {
             int r = tid + s * kHeatThreads;
             c.ro[s] = 0;
+            c.xr[s] = 0;
             c.rg[s] = 0;
             c.rf[s] = 0;
             c.rd[s] = -1;
@@ -441,6 +522,7 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
                     else { x = lo + side - 1; y = lo + 1 + (r - (3 * side - 2)); }
                     const long long gx = ix0 - kHeatH + x, gy = iy0 - kHeatH + y;
                     c.ro[s] = heat_sidx(x, y);
+                    c.xr[s] = y * kHeatW + x;
                     c.rf[s] = face_flags(gx, gy, g) | ((x & 1) ? kOdd : 0);
                     if (c.rf[s] & kIn) {
                         c.rg[s] = static_cast<int>(gy * g + gx);
@@ -460,17 +542,58 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
     const double* src = (field ? w.in1 : w.in0) - static_cast<long long>(w.win_begin) * g2;
     double* dst = (field ? w.out1 : w.out0) - static_cast<long long>(w.out_begin) * g2;
     const unsigned long long n_total = static_cast<unsigned long long>(g2 * g);
-    if (interior) {
-        HeatRun<Exact, true> r{hp, sc, c, smem, zs, ze, static_cast<int>(obz), static_cast<int>(oez),
-                               static_cast<int>(g), zs > 0, ze < g, g2, src, dst, field, m.method,
-                               step, fail, n_total};
-        r.run();
-    } else {
-        HeatRun<Exact, false> r{hp, sc, c, smem, zs, ze, static_cast<int>(obz), static_cast<int>(oez),
-                                static_cast<int>(g), zs > 0, ze < g, g2, src, dst, field, m.method,
-                                step, fail, n_total};
-        r.run();
+    if (tma) {
+        if (tid == 0) {
+            for (int s = 0; s < kHeatXRing; ++s) mbar_init(bars + s, 1);
+            mbar_fence_init();
+        }
+        __syncthreads();
     }
+    const void* tmap = &tm.f[field];
+    const int bx0 = static_cast<int>(ix0) - kHeatH, by0 = static_cast<int>(iy0) - kHeatH;
+    const int wbz = static_cast<int>(w.win_begin);
+#define PIRK_HEAT_RUN(INTERIOR, TMA)                                                               \
+    {                                                                                              \
+        HeatRun<Exact, INTERIOR, TMA> r{hp, sc, c, smem, zs, ze, static_cast<int>(obz),           \
+                                        static_cast<int>(oez), static_cast<int>(g), zs > 0, ze < g, \
+                                        g2, src, dst, field, m.method, step, fail, n_total, tmap,  \
+                                        bx0, by0, wbz, bars};                                      \
+        r.run();                                                                                   \
+    }
+    if (tma) {
+        if (interior) PIRK_HEAT_RUN(true, true) else PIRK_HEAT_RUN(false, true)
+    } else {
+        if (interior) PIRK_HEAT_RUN(true, false) else PIRK_HEAT_RUN(false, false)
+    }
+#undef PIRK_HEAT_RUN
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+inline bool heat_encode_tmap(CUtensorMap* out, const double* base, uint64_t g, uint64_t planes) {
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                CUtensorMapFloatOOBfill);
+    static Encode encode = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<Encode>(fn);
+    }
+    if (!encode) return false;
+    // strides must be 16-byte multiples and the base 16-byte aligned
+    if ((g * sizeof(double)) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) % 16) != 0) return false;
+    const cuuint64_t dims[3] = {g, g, planes};
+    const cuuint64_t strides[2] = {g * sizeof(double), g * g * sizeof(double)};
+    const cuuint32_t box[3] = {kHeatW, kHeatW, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <bool Exact>
@@ -501,7 +624,13 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
     const uint64_t zchunk = (planes + nchunks - 1) / nchunks;
     nchunks = (planes + zchunk - 1) / zchunk;
     dim3 grid(static_cast<unsigned>(tx), static_cast<unsigned>(tx), static_cast<unsigned>(2 * nchunks));
-    heat_step_kernel<Exact><<<grid, kHeatThreads, kHeatSmemBytes, stream>>>(m, hp, w, sc, step, zchunk, fail);
+    HeatTmaps tm;
+    std::memset(&tm, 0, sizeof tm);
+    const uint64_t wplanes = w.win_end - w.win_begin;
+    const int tma = heat_encode_tmap(&tm.f[0], w.in0, m.g, wplanes) &&
+                    heat_encode_tmap(&tm.f[1], w.in1, m.g, wplanes);
+    heat_step_kernel<Exact><<<grid, kHeatThreads, kHeatSmemBytes, stream>>>(m, hp, w, sc, step, zchunk,
+                                                                            fail, tm, tma);
     return cudaGetLastError();
 }
 

@@ -305,7 +305,7 @@ __device__ void hull_fold(const double* x, bool active, int n, unsigned long lon
 }
 
 template <bool Exact, int N>
-__global__ void __launch_bounds__(kMcThreads, 5)  // <= 102 registers: 20 warps/SM for the FP64 chains
+__global__ void __launch_bounds__(kMcThreads)
 monte_carlo_kernel(const SmallModel m, const McArgs a) {
     (void)sizeof(ModeCheck<Exact>);
     constexpr int NA = (N > 0) ? N : kSmallMax;
