@@ -55,8 +55,11 @@ constexpr int kHeatP = kHeatW + 1;           // 41: odd row pitch (bank-conflict
 constexpr int kHeatPlane = kHeatW * kHeatP;  // 1640
 constexpr int kHeatThreads = 512;            // one 1x2 own pair per thread
 constexpr int kHeatXRing = 8;                // x planes j-7 .. j (slot (p - zs) & 7)
-// x planes are row-major 40x40 (the TMA box), each slot padded to a 128-byte multiple
-constexpr int kHeatXSlot = 1664;             // >= 1600 doubles, 13,312 B
+// x planes are row-major with pitch 42 (the TMA box is 42 x 40: rows stay 16-byte
+// aligned as TMA requires, and 42 doubles = 20 banks mod 32 keeps column-wise
+// halo reads at most 2-way conflicted); slot = 1680 doubles = 105 x 128 B
+constexpr int kHeatXP = 42;
+constexpr int kHeatXSlot = kHeatXP * kHeatW;
 constexpr size_t kHeatSmemBytes =
     size_t(kHeatXRing) * kHeatXSlot * sizeof(double) + size_t(6) * kHeatPlane * sizeof(double);  // 185,216 B
 
@@ -207,7 +210,7 @@ struct HeatRun {
         double* X = S + xbuf(s);
         if constexpr (Tma) {
             if (threadIdx.x == 0) {
-                mbar_expect_tx(bars + s, kHeatW * kHeatW * sizeof(double));
+                mbar_expect_tx(bars + s, kHeatXSlot * sizeof(double));
                 tma_load_plane(X, tmap, bx0, by0, p - wbz, bars + s);
             }
         } else {
@@ -225,15 +228,19 @@ struct HeatRun {
                                                 double& k1) const {
         const double* B = S + x_off + c.xe;
         const double l = B[-1], r = B[2];
-        const double u0 = B[-kHeatW], u1 = B[1 - kHeatW];
-        const double d0 = B[kHeatW], d1 = B[kHeatW + 1];
-        k0 = heat_pt<Exact, Interior>(c0, l, c1, u0, d0, zm0, zp0, c.of[0], hp);
-        k1 = heat_pt<Exact, Interior>(c1, c0, r, u1, d1, zm1, zp1, c.of[1], hp);
+        const double2 u = *reinterpret_cast<const double2*>(B - kHeatXP);  // xe is even: aligned
+        const double2 d = *reinterpret_cast<const double2*>(B + kHeatXP);
+        k0 = heat_pt<Exact, Interior>(c0, l, c1, u.x, d.x, zm0, zp0, c.of[0], hp);
+        k1 = heat_pt<Exact, Interior>(c1, c0, r, u.y, d.y, zm1, zp1, c.of[1], hp);
     }
 
     __device__ __forceinline__ double ring_eval_x(double s, double zm, double zp, int x_off) const {
         const double* B = S + x_off + c.xr[0];
-        return heat_pt<Exact, Interior>(s, B[-1], B[1], B[-kHeatW], B[kHeatW], zm, zp, c.rf[0], hp);
+        return heat_pt<Exact, Interior>(s, B[-1], B[1], B[-kHeatXP], B[kHeatXP], zm, zp, c.rf[0], hp);
+    }
+
+    __device__ __forceinline__ double2 own_x(int x_off) const {
+        return *reinterpret_cast<const double2*>(S + x_off + c.xe);
     }
 
     // own pair: centres c0 (even col) and c1 (odd col) at level L-1 of plane p,
@@ -276,7 +283,8 @@ struct HeatRun {
         }
         if (j + 1 < ze) load(ldp, j + 1, (x8 + 1) & 7);  // x(j+1) into the slot of x(j-7)
         // own x(j): the z+ neighbour of stage 1
-        double xj0 = S[X0 + c.xe], xj1 = S[X0 + c.xe + 1];
+        const double2 xj = own_x(X0);
+        double xj0 = xj.x, xj1 = xj.y;
         double rxj = S[X0 + c.xr[0]];
         if (ZEdge && j == g) {  // insulated top face: x(g) := x(g-1)
             xj0 = ox[0][I1];
@@ -357,8 +365,9 @@ struct HeatRun {
                 pair_eval(ou2[0][I3], ou2[1][I3], ou2[0][I0], ou2[1][I0], ou2[0][I2], ou2[1][I2],
                           ubuf(2, P1), k0, k1);
                 // x(j-3) from the shared x ring (keeps the register budget at 128)
-                const double u0 = upd(S[X3 + c.xe], k0, sc.hk, hp.hkk);
-                const double u1 = upd(S[X3 + c.xe + 1], k1, sc.hk, hp.hkk);
+                const double2 x3 = own_x(X3);
+                const double u0 = upd(x3.x, k0, sc.hk, hp.hkk);
+                const double u1 = upd(x3.y, k1, sc.hk, hp.hkk);
                 ou3[0][I3] = u0;
                 ou3[1][I3] = u1;
                 oacc[0][I3] = fma(2.0, k0, oacc[0][I3]);
@@ -388,10 +397,12 @@ struct HeatRun {
                           ubuf(3, P0), k0, k1);
                 double* out = stp;
                 const double kk[2] = {k0, k1};
+                const double2 x4 = own_x(X4);  // x(j-4)
+                const double xs[2] = {x4.x, x4.y};
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
                     if (!in(k)) continue;
-                    const double x = S[X4 + c.xe + k];  // x(j-4)
+                    const double x = xs[k];
                     const double xn = Exact ? x + sc.h6 * (oacc[k][I0] + kk[k])
                                             : fma(hp.h6kk, oacc[k][I0] + kk[k], x);
                     out[c.og + k] = xn;
@@ -495,7 +506,7 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
     {
         const int bx = tid & 15, by = tid >> 4;           // own pair (2bx, by) in tile coords
         c.oe = heat_sidx(2 * bx + kHeatH, by + kHeatH);
-        c.xe = (by + kHeatH) * kHeatW + (2 * bx + kHeatH);
+        c.xe = (by + kHeatH) * kHeatXP + (2 * bx + kHeatH);
         const long long ix = ix0 + 2 * bx, iy = iy0 + by;
         c.of[0] = face_flags(ix, iy, g);
         c.of[1] = face_flags(ix + 1, iy, g);
@@ -522,7 +533,7 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
                     else { x = lo + side - 1; y = lo + 1 + (r - (3 * side - 2)); }
                     const long long gx = ix0 - kHeatH + x, gy = iy0 - kHeatH + y;
                     c.ro[s] = heat_sidx(x, y);
-                    c.xr[s] = y * kHeatW + x;
+                    c.xr[s] = y * kHeatXP + x;
                     c.rf[s] = face_flags(gx, gy, g) | ((x & 1) ? kOdd : 0);
                     if (c.rf[s] & kIn) {
                         c.rg[s] = static_cast<int>(gy * g + gx);
@@ -589,7 +600,7 @@ inline bool heat_encode_tmap(CUtensorMap* out, const double* base, uint64_t g, u
     if ((g * sizeof(double)) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) % 16) != 0) return false;
     const cuuint64_t dims[3] = {g, g, planes};
     const cuuint64_t strides[2] = {g * sizeof(double), g * g * sizeof(double)};
-    const cuuint32_t box[3] = {kHeatW, kHeatW, 1};
+    const cuuint32_t box[3] = {kHeatXP, kHeatW, 1};
     const cuuint32_t es[3] = {1, 1, 1};
     return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
