@@ -172,6 +172,12 @@ struct HeatCols {
     int rg[2];     // in-plane global offset
     int rf[2];     // face flags (| kOdd)
     int rd[2];     // number of stages computed at the column (0..3; -1: none)
+    // Warp-uniform max of rd[0]: ring stage L runs in every lane of a warp that
+    // has any lane needing it.  A lane computing a level beyond its column's
+    // depth only writes shared cells (and its own registers) that no stage
+    // reads: a level-L value at distance d > 4-L is never a neighbour of a
+    // level-(L+1) evaluation (those sit at distance <= 3-L).
+    int wd;
 };
 
 template <bool Exact, bool Interior, bool Tma>
@@ -310,7 +316,7 @@ struct HeatRun {
                     ou1[0][I2] = u0;
                     ou1[1][I2] = u1;
                 }
-                if (c.rd[0] >= 1) {
+                if (c.wd >= 1) {
                     const double s = rx[I1];
                     const double kr = ring_eval_x(s, rx[I2], rxj, X1);
                     const double uu = upd(s, kr, sc.h2, hp.h2kk);
@@ -343,7 +349,7 @@ struct HeatRun {
                     ou2[0][I3] = u0;
                     ou2[1][I3] = u1;
                 }
-                if (c.rd[0] >= 2) {
+                if (c.wd >= 2) {
                     const double s = ru1[I2];
                     const double kr = ring_eval(s, ru1[I3], ru1[I1], ubuf(1, P0));
                     const double uu = upd(rx[I2], kr, sc.h2, hp.h2kk);
@@ -378,7 +384,7 @@ struct HeatRun {
                     ou3[0][I0] = u0;
                     ou3[1][I0] = u1;
                 }
-                if (c.rd[0] >= 3) {
+                if (c.wd >= 3) {
                     const double s = ru2[I3];
                     const double kr = ring_eval(s, ru2[I0], ru2[I2], ubuf(2, P1));
                     S[ubuf(3, P1) + c.ro[0]] = upd(S[X3 + c.xr[0]], kr, sc.hk, hp.hkk);
@@ -399,14 +405,19 @@ struct HeatRun {
                 const double kk[2] = {k0, k1};
                 const double2 x4 = own_x(X4);  // x(j-4)
                 const double xs[2] = {x4.x, x4.y};
+                double xn[2];
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
-                    if (!in(k)) continue;
-                    const double x = xs[k];
-                    const double xn = Exact ? x + sc.h6 * (oacc[k][I0] + kk[k])
-                                            : fma(hp.h6kk, oacc[k][I0] + kk[k], x);
-                    out[c.og + k] = xn;
-                    if (!finite_d(xn)) {
+                    xn[k] = Exact ? xs[k] + sc.h6 * (oacc[k][I0] + kk[k])
+                                  : fma(hp.h6kk, oacc[k][I0] + kk[k], xs[k]);
+                    if (in(k)) out[c.og + k] = xn[k];
+                }
+                // one test per pair: the sum is non-finite whenever either value
+                // is (a finite overflow only sends the pair to the exact check)
+                if (!finite_d(xn[0] + xn[1])) {
+#pragma unroll
+                    for (int k = 0; k < 2; ++k) {
+                        if (!in(k) || finite_d(xn[k])) continue;
                         const unsigned long long gi = static_cast<unsigned long long>(
                             static_cast<long long>(p) * g2 + c.og + k);
                         if (method == 0)
@@ -517,12 +528,17 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
             int r = tid + s * kHeatThreads;
+            // the computed bands (d = 1..3) fill ring indices [0, 420); the
+            // load-only band d = 4 starts at the warp boundary 448 so that no
+            // warp mixes the two (see HeatCols::wd)
+            constexpr int kComputed = 132 + 140 + 148, kLoadStart = 448;
+            if (r >= kComputed) r = (r < kLoadStart) ? -1 : r - kLoadStart + kComputed;
             c.ro[s] = 0;
             c.xr[s] = 0;
             c.rg[s] = 0;
             c.rf[s] = 0;
             c.rd[s] = -1;
-            for (int d = 1; d <= kHeatH; ++d) {
+            for (int d = 1; d <= kHeatH && r >= 0; ++d) {
                 const int side = kHeatT + 2 * d, cnt = 4 * side - 4;
                 if (r < cnt) {
                     const int lo = kHeatH - d;  // footprint coordinate of the band's first row/col
@@ -545,6 +561,7 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
             }
         }
     }
+    c.wd = __reduce_max_sync(0xffffffffu, c.rd[0]);
     const bool interior = ix0 - kHeatH >= 0 && ix0 + kHeatT + kHeatH <= g && iy0 - kHeatH >= 0 &&
                           iy0 + kHeatT + kHeatH <= g;
     const long long g2 = g * g;
