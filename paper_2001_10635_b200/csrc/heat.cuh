@@ -129,6 +129,43 @@ __device__ __forceinline__ void tma_load_plane(double* dst, const void* tmap, in
         : "memory");
 }
 
+// TMEM as per-thread pipeline storage: each warp owns a 32-lane quadrant
+// (warp % 4) and a 128-column slice (warp / 4) of the CTA's 512 columns; a
+// thread keeps its two RK accumulators per plane in flight there (4 planes x
+// 2 doubles = 16 columns), freeing registers for the stencil pipeline.
+__device__ __forceinline__ void tmem_alloc512(unsigned* dst) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(dst))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc512(unsigned taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(taddr) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+// No "memory" clobbers: TMEM is not compiler-visible memory, and volatile asm
+// statements keep their relative order (st before a later ld of the slot), so
+// shared-memory loads remain free to be scheduled across these.
+__device__ __forceinline__ void tmem_st2(unsigned taddr, double a, double b) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(taddr),
+                 "r"(__double2loint(a)), "r"(__double2hiint(a)), "r"(__double2loint(b)),
+                 "r"(__double2hiint(b)));
+}
+__device__ __forceinline__ void tmem_ld2(unsigned taddr, double& a, double& b) {
+    unsigned r0, r1, r2, r3;
+    asm volatile("tcgen05.wait::st.sync.aligned;\n");
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" : "+r"(r0), "+r"(r1), "+r"(r2), "+r"(r3));
+    a = __hiloint2double(static_cast<int>(r1), static_cast<int>(r0));
+    b = __hiloint2double(static_cast<int>(r3), static_cast<int>(r2));
+}
+
 // Stencil value from the six neighbours.  Exact: k = kk*acc.  Fast: t = sum - 6 s.
 template <bool Exact, bool Interior>
 __device__ __forceinline__ double heat_pt(double s, double xm, double xp, double ym, double yp,
@@ -200,7 +237,15 @@ struct HeatRun {
     unsigned long long* bars;
 
     // register state: slot (p - zs) & 3 of plane p
-    double ox[2][4], ou1[2][4], ou2[2][4], ou3[2][4], oacc[2][4];
+    double ox[2][4], ou1[2][4], ou2[2][4], ou3[2][4];
+    unsigned tacc;   // TMEM address of this thread's accumulator slots (4 columns per plane slot)
+
+    __device__ __forceinline__ void acc_st(int slot, double a, double b) const {
+        tmem_st2(tacc + 4 * slot, a, b);
+    }
+    __device__ __forceinline__ void acc_ld(int slot, double& a, double& b) const {
+        tmem_ld2(tacc + 4 * slot, a, b);
+    }
     double rx[4], ru1[4], ru2[4];   // ring slot 0 (depth <= 3)
 
     __device__ __forceinline__ bool in(int k) const { return Interior || (c.of[k] & kIn); }
@@ -287,7 +332,12 @@ struct HeatRun {
         if constexpr (Tma) {
             if (j < ze) mbar_wait(bars + x8, ((j - zs) >> 3) & 1);  // x(j) landed
         }
-        if (j + 1 < ze) load(ldp, j + 1, (x8 + 1) & 7);  // x(j+1) into the slot of x(j-7)
+        if constexpr (Tma) {
+            // two planes of prefetch: x(j+2) into the slot of x(j-6), last read in iteration j-2
+            if (j + 2 < ze) load(nullptr, j + 2, (x8 + 2) & 7);
+        } else {
+            if (j + 1 < ze) load(ldp, j + 1, (x8 + 1) & 7);  // x(j+1) into the slot of x(j-7)
+        }
         // own x(j): the z+ neighbour of stage 1
         const double2 xj = own_x(X0);
         double xj0 = xj.x, xj1 = xj.y;
@@ -308,8 +358,7 @@ struct HeatRun {
                 const double u1 = upd(ox[1][I1], k1, sc.h2, hp.h2kk);
                 ou1[0][I1] = u0;
                 ou1[1][I1] = u1;
-                oacc[0][I1] = k0;
-                oacc[1][I1] = k1;
+                acc_st(I1, k0, k1);
                 S[ubuf(1, P1) + c.oe] = u0;
                 S[ubuf(1, P1) + c.oe + kHeatHalf] = u1;
                 if (ZEdge && p == 0) {  // insulated bottom face: u1(-1) := u1(0)
@@ -341,8 +390,9 @@ struct HeatRun {
                 const double u1 = upd(ox[1][I2], k1, sc.h2, hp.h2kk);
                 ou2[0][I2] = u0;
                 ou2[1][I2] = u1;
-                oacc[0][I2] = fma(2.0, k0, oacc[0][I2]);  // acc + 2k (exact: 2k is exact)
-                oacc[1][I2] = fma(2.0, k1, oacc[1][I2]);
+                double a0, a1;
+                acc_ld(I2, a0, a1);
+                acc_st(I2, fma(2.0, k0, a0), fma(2.0, k1, a1));  // acc + 2k (exact: 2k is exact)
                 S[ubuf(2, P0) + c.oe] = u0;
                 S[ubuf(2, P0) + c.oe + kHeatHalf] = u1;
                 if (ZEdge && p == 0) {
@@ -376,8 +426,9 @@ struct HeatRun {
                 const double u1 = upd(x3.y, k1, sc.hk, hp.hkk);
                 ou3[0][I3] = u0;
                 ou3[1][I3] = u1;
-                oacc[0][I3] = fma(2.0, k0, oacc[0][I3]);
-                oacc[1][I3] = fma(2.0, k1, oacc[1][I3]);
+                double a0, a1;
+                acc_ld(I3, a0, a1);
+                acc_st(I3, fma(2.0, k0, a0), fma(2.0, k1, a1));
                 S[ubuf(3, P1) + c.oe] = u0;
                 S[ubuf(3, P1) + c.oe + kHeatHalf] = u1;
                 if (ZEdge && p == 0) {
@@ -405,11 +456,12 @@ struct HeatRun {
                 const double kk[2] = {k0, k1};
                 const double2 x4 = own_x(X4);  // x(j-4)
                 const double xs[2] = {x4.x, x4.y};
-                double xn[2];
+                double xn[2], acc[2];
+                acc_ld(I0, acc[0], acc[1]);
 #pragma unroll
                 for (int k = 0; k < 2; ++k) {
-                    xn[k] = Exact ? xs[k] + sc.h6 * (oacc[k][I0] + kk[k])
-                                  : fma(hp.h6kk, oacc[k][I0] + kk[k], xs[k]);
+                    xn[k] = Exact ? xs[k] + sc.h6 * (acc[k] + kk[k])
+                                  : fma(hp.h6kk, acc[k] + kk[k], xs[k]);
                     if (in(k)) out[c.og + k] = xn[k];
                 }
                 // one test per pair: the sum is non-finite whenever either value
@@ -456,6 +508,9 @@ struct HeatRun {
     __device__ __forceinline__ void run() {
         if (zs < ze) {
             load(src + static_cast<long long>(zs) * g2, zs, 0);  // x(zs) -> slot 0
+            if constexpr (Tma) {
+                if (zs + 1 < ze) load(nullptr, zs + 1, 1);       // x(zs+1) -> slot 1
+            }
             if constexpr (!Tma) cp_async_wait_all();
         }
         __syncthreads();
@@ -570,13 +625,18 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
     const double* src = (field ? w.in1 : w.in0) - static_cast<long long>(w.win_begin) * g2;
     double* dst = (field ? w.out1 : w.out0) - static_cast<long long>(w.out_begin) * g2;
     const unsigned long long n_total = static_cast<unsigned long long>(g2 * g);
-    if (tma) {
-        if (tid == 0) {
-            for (int s = 0; s < kHeatXRing; ++s) mbar_init(bars + s, 1);
-            mbar_fence_init();
-        }
-        __syncthreads();
+    __shared__ unsigned tmem_base;
+    const int warp = tid >> 5;
+    if (warp == 0) tmem_alloc512(&tmem_base);  // one CTA per SM: the 512 columns are free
+    if (tma && tid == 0) {
+        for (int s = 0; s < kHeatXRing; ++s) mbar_init(bars + s, 1);
+        mbar_fence_init();
     }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const unsigned tacc = tmem_base + (static_cast<unsigned>(32 * (warp & 3)) << 16) +
+                          static_cast<unsigned>(128 * (warp >> 2));
     const void* tmap = &tm.f[field];
     const int bx0 = static_cast<int>(ix0) - kHeatH, by0 = static_cast<int>(iy0) - kHeatH;
     const int wbz = static_cast<int>(w.win_begin);
@@ -586,6 +646,7 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
                                         static_cast<int>(oez), static_cast<int>(g), zs > 0, ze < g, \
                                         g2, src, dst, field, m.method, step, fail, n_total, tmap,  \
                                         bx0, by0, wbz, bars};                                      \
+        r.tacc = tacc;                                                                             \
         r.run();                                                                                   \
     }
     if (tma) {
@@ -594,6 +655,11 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
         if (interior) PIRK_HEAT_RUN(true, false) else PIRK_HEAT_RUN(false, false)
     }
 #undef PIRK_HEAT_RUN
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc512(tmem_base);
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
