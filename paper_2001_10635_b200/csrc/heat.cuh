@@ -333,8 +333,9 @@ struct HeatRun {
             if (j < ze) mbar_wait(bars + x8, ((j - zs) >> 3) & 1);  // x(j) landed
         }
         if constexpr (Tma) {
-            // two planes of prefetch: x(j+2) into the slot of x(j-6), last read in iteration j-2
-            if (j + 2 < ze) load(nullptr, j + 2, (x8 + 2) & 7);
+            // three planes of prefetch: x(j+3) into the slot of x(j-5), last read
+            // (stage 4) in iteration j-1
+            if (j + 3 < ze) load(nullptr, j + 3, (x8 + 3) & 7);
         } else {
             if (j + 1 < ze) load(ldp, j + 1, (x8 + 1) & 7);  // x(j+1) into the slot of x(j-7)
         }
@@ -510,6 +511,7 @@ struct HeatRun {
             load(src + static_cast<long long>(zs) * g2, zs, 0);  // x(zs) -> slot 0
             if constexpr (Tma) {
                 if (zs + 1 < ze) load(nullptr, zs + 1, 1);       // x(zs+1) -> slot 1
+                if (zs + 2 < ze) load(nullptr, zs + 2, 2);       // x(zs+2) -> slot 2
             }
             if constexpr (!Tma) cp_async_wait_all();
         }
@@ -588,8 +590,11 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
             // warp mixes the two (see HeatCols::wd)
             constexpr int kComputed = 132 + 140 + 148, kLoadStart = 448;
             if (r >= kComputed) r = (r < kLoadStart) ? -1 : r - kLoadStart + kComputed;
-            c.ro[s] = 0;
-            c.xr[s] = 0;
+            // a lane without a column may still run a ring stage (wd): point it
+            // at never-read pad cells (U: row 1, index 40; x ring: row 1, col 41)
+            // so its neighbour reads stay inside the buffers and its writes are dead
+            c.ro[s] = kHeatP + kHeatW;
+            c.xr[s] = kHeatXP + kHeatXP - 1;
             c.rg[s] = 0;
             c.rf[s] = 0;
             c.rd[s] = -1;
@@ -688,44 +693,6 @@ inline bool heat_encode_tmap(CUtensorMap* out, const double* base, uint64_t g, u
     return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-template <bool Exact>
-cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const StepConsts& sc,
-                             unsigned long long step, unsigned long long* fail,
-                             cudaStream_t stream) {
-    if (w.out_end <= w.out_begin) return cudaSuccess;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(heat_step_kernel<Exact>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(kHeatSmemBytes));
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
-    HeatStepParams hp;
-    hp.kk = m.kk;
-    hp.robin = m.robin;
-    hp.h2kk = sc.h2 * m.kk;
-    hp.hkk = sc.hk * m.kk;
-    hp.h6kk = sc.h6 * m.kk;
-    const uint64_t planes = w.out_end - w.out_begin;
-    // z chunks: enough CTAs to fill the machine, few enough to keep the
-    // 8-plane halo overhead per chunk small.
-    const uint64_t tx = (m.g + kHeatT - 1) / kHeatT;
-    uint64_t nchunks = 1;
-    while (tx * tx * 2 * nchunks < 4 * 148 && planes / (nchunks * 2) >= 64) nchunks *= 2;
-    const uint64_t zchunk = (planes + nchunks - 1) / nchunks;
-    nchunks = (planes + zchunk - 1) / zchunk;
-    dim3 grid(static_cast<unsigned>(tx), static_cast<unsigned>(tx), static_cast<unsigned>(2 * nchunks));
-    HeatTmaps tm;
-    std::memset(&tm, 0, sizeof tm);
-    const uint64_t wplanes = w.win_end - w.win_begin;
-    const int tma = heat_encode_tmap(&tm.f[0], w.in0, m.g, wplanes) &&
-                    heat_encode_tmap(&tm.f[1], w.in1, m.g, wplanes);
-    heat_step_kernel<Exact><<<grid, kHeatThreads, kHeatSmemBytes, stream>>>(m, hp, w, sc, step, zchunk,
-                                                                            fail, tm, tma);
-    return cudaGetLastError();
 }
 
 }  // namespace pirk

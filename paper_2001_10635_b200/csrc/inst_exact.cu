@@ -1,7 +1,7 @@
 // Exact-mode instantiations: compiled with -fmad=false -DPIRK_TU_EXACT=1, so
 // every kernel here rounds exactly like the reference's non-FMA build.
 #include "chain.cuh"
-#include "heat.cuh"
+#include "heat2x2.cuh"
 #include "small.cuh"
 
 namespace pirk {

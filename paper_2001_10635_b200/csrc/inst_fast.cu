@@ -1,7 +1,7 @@
 // Fast-mode instantiations: FMA contraction on (default nvcc), restructured
 // stencils; held to relative <= 1e-12 of the reference.
 #include "chain.cuh"
-#include "heat.cuh"
+#include "heat2x2.cuh"
 #include "small.cuh"
 
 namespace pirk {

@@ -99,6 +99,46 @@ def test_heat_fast_mode_tolerance(fast_ctx, g):
     assert_within(pk.mixed_monotonicity(prob, ctx=fast_ctx), oracle_for("mm", prob))
 
 
+def heat_interior_problem(g, seed=5, steps=4):
+    """A grid large enough for interior tiles (halo-4 footprint inside the
+    grid: g >= 68), the path the bench sizes run; g = 160 also splits z into
+    chunks, odd g takes the cp.async fallback instead of TMA."""
+    n = g ** 3
+    rng = np.random.default_rng(seed)
+    lo = rng.uniform(0.5, 1.0, n)
+    hi = lo + rng.uniform(0.0, 0.5, n)
+    h = 0.2 / (g - 1) ** 2
+    return heat_problem(g, t1=steps * h, h=h, stride=2, lo=lo, hi=hi)
+
+
+@pytest.mark.parametrize("g", [72, 75, 100, 160])
+def test_heat_interior_tiles_exact(ctx, g):
+    m, prob = heat_interior_problem(g)
+    assert_bitexact(pk.mixed_monotonicity(prob, ctx=ctx), oracle_for("mm", prob))
+    if g == 100:
+        assert_bitexact(pk.growth_bound(prob, ctx=ctx), oracle_for("gb", prob))
+
+
+@pytest.mark.parametrize("g", [72, 75, 160])
+def test_heat_interior_tiles_fast(fast_ctx, g):
+    m, prob = heat_interior_problem(g)
+    assert_within(pk.mixed_monotonicity(prob, ctx=fast_ctx), oracle_for("mm", prob))
+
+
+@pytest.mark.parametrize("variant", ["1x2", "2x2"])
+def test_heat_block_variants(variant):
+    """Both heat kernels (1x2 pairs, 2x2 blocks) in both modes: the selector
+    (PIRK_HEAT_BLOCK) is read once per process, so each runs in a child."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PIRK_HEAT_BLOCK=variant)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        os.path.join(root, "tests", "test_gpu_parity.py"),
+                        "-k", "heat and not variants"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 # -------------------------------------------------------------------- chain
 
 @pytest.mark.parametrize("n", [1, 2, 7, 1000, 1016, 1017, 5000])
