@@ -308,11 +308,13 @@ def run_ours(args):
     launch_bytes = 16.0 * 2 * n / world
     achieved = launch_bytes / (per_launch_ms * 1e-3) / 1e9
     traffic = None
+    # dominant kernel by mode (heat2x2.cuh launch_heat_step): 2x2 blocks in fast mode
+    kernel = "heat2_step_kernel" if args.mode == "fast" else "heat_step_kernel"
     tp = os.path.join(ROOT, "profiles", "heat_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             tj = json.load(f).get(args.mode)
-        if tj:
+        if tj and tj.get("kernel") == kernel:
             traffic = tj["dram_bytes_per_update"] * 2 * n / world
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -327,7 +329,7 @@ def run_ours(args):
         "clocks": clocks,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "peak_source": how,
-                     "kernel": "heat_step_kernel", "algorithmic_bytes_per_launch": launch_bytes,
+                     "kernel": kernel, "algorithmic_bytes_per_launch": launch_bytes,
                      "avg_launch_ms": per_launch_ms},
         "finite": ok,
     }

@@ -40,6 +40,7 @@
 
 #include <cuda.h>  // CUtensorMap (encoded through cudaGetDriverEntryPoint)
 
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -690,9 +691,21 @@ inline bool heat_encode_tmap(CUtensorMap* out, const double* base, uint64_t g, u
     const cuuint64_t strides[2] = {g * sizeof(double), g * g * sizeof(double)};
     const cuuint32_t box[3] = {kHeatXP, kHeatW, 1};
     const cuuint32_t es[3] = {1, 1, 1};
+    // L2 fill granularity of the box loads: a box row is 336 B at a 32 B
+    // misalignment, so 64 B fills fetch the least from DRAM (measured, g=800:
+    // 9.95 GB read per launch vs 12.08 GB at 256 B).  PIRK_TMA_PROMO overrides.
+    static const CUtensorMapL2promotion promo = [] {
+        const char* v = std::getenv("PIRK_TMA_PROMO");
+        if (!v) return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+        const int b = std::atoi(v);
+        return b == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+               : b == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+               : b == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                          : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    }();
     return encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides,
                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+                  promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace pirk
