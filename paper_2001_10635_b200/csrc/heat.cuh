@@ -6,22 +6,28 @@
 // (growth_rhs == rhs for heat3d, models.cpp:130).
 //
 // Design: 2.5-D z-streaming with register-resident z histories.
-//   A CTA of 512 threads owns a 32x32 x-y tile of one field and streams the
-//   planes of a z-chunk.  Iteration j issues cp.async loads of x-plane j+1
-//   (tile + halo 4) into a 4-slot shared ring and evaluates stage 1 at plane
-//   j-1, stage 2 at j-2, stage 3 at j-3 and stage 4 (the RK4 combination,
-//   stored to HBM) at j-4.  Every (x, y) column of the 40x40 footprint belongs
-//   to one thread for the whole run, so a column's values at neighbouring
-//   planes (the z+-1 terms), its RK accumulator and its x for the stage
-//   updates stay in that thread's registers.  Shared memory carries only the
-//   in-plane (x+-1, y+-1) exchange: u1/u2/u3 planes double-buffered, each
-//   stage reading the plane its predecessor wrote in the previous iteration --
-//   one __syncthreads per plane.  Rows have an odd pitch (41 doubles) with
-//   even and odd columns de-interleaved, so both row-wise and column-wise
-//   neighbour loads of a warp are bank-conflict free.  Own points are 1x2
+//   A CTA (one per SM: 185 KB of shared memory) owns a 32x32 x-y tile of one
+//   field and streams the planes of a z-chunk.  Iteration j waits for x-plane
+//   j (tile + halo 4, a 42x40 TMA box with out-of-grid cells zero-filled,
+//   completing on an mbarrier), issues the TMA load of plane j+3 into an
+//   8-slot ring, and evaluates stage 1 at plane j-1, stage 2 at j-2, stage 3
+//   at j-3 and stage 4 (the RK4 combination, stored to HBM) at j-4.  Every
+//   (x, y) column of the 40x40 footprint belongs to one thread for the whole
+//   run, so a column's values at neighbouring planes (the z+-1 terms) stay in
+//   that thread's registers; its RK accumulators live in TMEM (tcgen05.st/ld,
+//   one 32-lane quadrant per warp), which keeps the kernel spill-free.
+//   Shared memory carries only the in-plane (x+-1, y+-1) exchange: u1/u2/u3
+//   planes double-buffered, each stage reading the plane its predecessor
+//   wrote in the previous iteration -- one __syncthreads per plane.  u rows
+//   have an odd pitch (41 doubles) with even and odd columns de-interleaved,
+//   so row-wise and column-wise neighbour loads of a warp are bank-conflict
+//   free; x planes are row-major (pitch 42, the TMA box).  Own points are 1x2
 //   register pairs (the pair's inner neighbours come from registers); the 576
-//   halo-ring columns are single points (one or two per thread).  HBM sees
-//   each x once and each x' once: 16 B per state-update.
+//   halo-ring columns are single points (one or two per thread), grouped by
+//   depth so that ring stages branch per warp, not per lane.  HBM sees each x
+//   once and each x' once: 16 B per state-update (plus halo re-reads that
+//   miss L2; profiles/heat_traffic.json).  heat2x2.cuh is the 2x2-block
+//   variant of this kernel (the fast-mode default).
 //
 // Boundaries.  Interior tiles (halo-4 footprint inside the grid in x and y)
 // run without per-point checks.  Insulated z faces: the history slot of the
