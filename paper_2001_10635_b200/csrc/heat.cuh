@@ -73,6 +73,9 @@ constexpr size_t kHeatSmemBytes =
 struct HeatStepParams {
     double kk, robin;
     double h2kk, hkk, h6kk;  // fast-mode folded constants
+    // fast-mode Horner coefficients hk*kk/4, /3, /2, /1 (heat2x2.cuh): for a
+    // linear autonomous field RK4 is x + hL(x + hL/2(x + hL/3(x + hL/4 x)))
+    double hn[4];
 };
 
 // face flags (edge tiles); kOdd marks an odd footprint column (neighbour offsets)

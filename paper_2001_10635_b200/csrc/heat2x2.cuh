@@ -144,6 +144,16 @@ struct Heat2Run {
                                               const double (&zp)[4], double l0, double r0, double l1,
                                               double r1, double u0, double u1, double d0, double d1,
                                               double (&k)[4]) const {
+        if constexpr (!Exact && Interior) {
+            // fast interior: (ce1 + ce2) is in the sums of points 0 and 3,
+            // (ce0 + ce3) in those of points 1 and 2
+            const double a = ce[1] + ce[2], b = ce[0] + ce[3];
+            k[0] = fma(-6.0, ce[0], (a + (l0 + u0)) + (zm[0] + zp[0]));
+            k[1] = fma(-6.0, ce[1], (b + (r0 + u1)) + (zm[1] + zp[1]));
+            k[2] = fma(-6.0, ce[2], (b + (l1 + d0)) + (zm[2] + zp[2]));
+            k[3] = fma(-6.0, ce[3], (a + (r1 + d1)) + (zm[3] + zp[3]));
+            return;
+        }
         k[0] = heat_pt<Exact, Interior>(ce[0], l0, ce[1], u0, ce[2], zm[0], zp[0], c.of[0], hp);
         k[1] = heat_pt<Exact, Interior>(ce[1], ce[0], r0, u1, ce[3], zm[1], zp[1], c.of[1], hp);
         k[2] = heat_pt<Exact, Interior>(ce[2], l1, ce[3], ce[0], d0, zm[2], zp[2], c.of[2], hp);
@@ -229,22 +239,22 @@ struct Heat2Run {
                 block_eval_x(ce, zm, xj, X1, kv);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    u[k] = upd(ce[k], kv[k], sc.h2, hp.h2kk);
+                    u[k] = upd(ce[k], kv[k], sc.h2, hp.hn[0]);
                     ou1[k][I1] = u[k];
                     if (ZEdge && p == 0) ou1[k][I2] = u[k];  // u1(-1) := u1(0)
                 }
-                tmem_st4(tacc + 8 * I1, kv);
+                if constexpr (Exact) tmem_st4(tacc + 8 * I1, kv);
                 block_store(ubuf(1, P1), u);
                 {  // slot 0 spans ring indices 0..255 (bands d = 1, 2): every warp runs stages 1-2
                     const double s = rx[I1];
-                    const double uu = upd(s, ring_eval_x<0>(s, rx[I2], rxj, X1), sc.h2, hp.h2kk);
+                    const double uu = upd(s, ring_eval_x<0>(s, rx[I2], rxj, X1), sc.h2, hp.hn[0]);
                     ru1[I1] = uu;
                     S[ubuf(1, P1) + c.ro[0]] = uu;
                     if (ZEdge && p == 0) ru1[I2] = uu;
                 }
                 if (c.wd[1] >= 1) {
                     const double s = sx[I1];
-                    const double uu = upd(s, ring_eval_x<1>(s, sx[I2], sxj, X1), sc.h2, hp.h2kk);
+                    const double uu = upd(s, ring_eval_x<1>(s, sx[I2], sxj, X1), sc.h2, hp.hn[0]);
                     su1[I1] = uu;
                     S[ubuf(1, P1) + c.ro[1]] = uu;
                     if (ZEdge && p == 0) su1[I2] = uu;
@@ -268,26 +278,26 @@ struct Heat2Run {
                     zp[k] = ou1[k][I1];
                 }
                 block_eval(ce, zm, zp, ubuf(1, P0), kv);
-                tmem_ld4(tacc + 8 * I2, a);
+                if constexpr (Exact) tmem_ld4(tacc + 8 * I2, a);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    u[k] = upd(ox[k][I2], kv[k], sc.h2, hp.h2kk);
+                    u[k] = upd(ox[k][I2], kv[k], sc.h2, hp.hn[1]);
                     ou2[k][I2] = u[k];
                     if (ZEdge && p == 0) ou2[k][I3] = u[k];
-                    a[k] = fma(2.0, kv[k], a[k]);  // acc + 2k (exact: 2k is exact)
+                    if constexpr (Exact) a[k] = fma(2.0, kv[k], a[k]);  // acc + 2k (2k is exact)
                 }
-                tmem_st4(tacc + 8 * I2, a);
+                if constexpr (Exact) tmem_st4(tacc + 8 * I2, a);
                 block_store(ubuf(2, P0), u);
                 {
                     const double uu = upd(rx[I2], ring_eval<0>(ru1[I2], ru1[I3], ru1[I1], ubuf(1, P0)),
-                                          sc.h2, hp.h2kk);
+                                          sc.h2, hp.hn[1]);
                     ru2[I2] = uu;
                     S[ubuf(2, P0) + c.ro[0]] = uu;
                     if (ZEdge && p == 0) ru2[I3] = uu;
                 }
                 if (c.wd[1] >= 2) {
                     S[ubuf(2, P0) + c.ro[1]] =
-                        upd(sx[I2], ring_eval<1>(su1[I2], su1[I3], su1[I1], ubuf(1, P0)), sc.h2, hp.h2kk);
+                        upd(sx[I2], ring_eval<1>(su1[I2], su1[I3], su1[I1], ubuf(1, P0)), sc.h2, hp.hn[1]);
                 }
             } else if (ZEdge && p == g) {
 #pragma unroll
@@ -307,19 +317,23 @@ struct Heat2Run {
                     zp[k] = ou2[k][I2];
                 }
                 block_eval(ce, zm, zp, ubuf(2, P1), kv);
-                tmem_ld4x2(tacc + 8 * I3, tacc + kXHist + 8 * I3, a, x3);  // acc, x(j-3)
+                if constexpr (Exact) {
+                    tmem_ld4x2(tacc + 8 * I3, tacc + kXHist + 8 * I3, a, x3);  // acc, x(j-3)
+                } else {
+                    tmem_ld4(tacc + kXHist + 8 * I3, x3);  // x(j-3)
+                }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    u[k] = upd(x3[k], kv[k], sc.hk, hp.hkk);
+                    u[k] = upd(x3[k], kv[k], sc.hk, hp.hn[2]);
                     ou3[k][I3] = u[k];
                     if (ZEdge && p == 0) ou3[k][I0] = u[k];
-                    a[k] = fma(2.0, kv[k], a[k]);
+                    if constexpr (Exact) a[k] = fma(2.0, kv[k], a[k]);
                 }
-                tmem_st4(tacc + 8 * I3, a);
+                if constexpr (Exact) tmem_st4(tacc + 8 * I3, a);
                 block_store(ubuf(3, P1), u);
                 if (c.wd[0] >= 3) {
                     S[ubuf(3, P1) + c.ro[0]] = upd(
-                        rx[I3], ring_eval<0>(ru2[I3], ru2[I0], ru2[I2], ubuf(2, P1)), sc.hk, hp.hkk);
+                        rx[I3], ring_eval<0>(ru2[I3], ru2[I0], ru2[I2], ubuf(2, P1)), sc.hk, hp.hn[2]);
                 }
             } else if (ZEdge && p == g) {
 #pragma unroll
@@ -338,10 +352,15 @@ struct Heat2Run {
                     zp[k] = ou3[k][I3];
                 }
                 block_eval(ce, zm, zp, ubuf(3, P0), kv);
-                tmem_ld4x2(tacc + 8 * I0, tacc + kXHist + 8 * I0, a, x4);  // acc, x(j-4)
+                if constexpr (Exact) {
+                    tmem_ld4x2(tacc + 8 * I0, tacc + kXHist + 8 * I0, a, x4);  // acc, x(j-4)
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    xn[k] = Exact ? x4[k] + sc.h6 * (a[k] + kv[k]) : fma(hp.h6kk, a[k] + kv[k], x4[k]);
+                    for (int k = 0; k < 4; ++k) xn[k] = x4[k] + sc.h6 * (a[k] + kv[k]);
+                } else {
+                    tmem_ld4(tacc + kXHist + 8 * I0, x4);  // x(j-4)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) xn[k] = fma(hp.hn[3], kv[k], x4[k]);
+                }
                 double* out = stp + c.og;
                 if (Interior && vec) {  // og even: 16-byte aligned pairs
                     *reinterpret_cast<double2*>(out) = make_double2(xn[0], xn[1]);
@@ -576,6 +595,10 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
     hp.h2kk = sc.h2 * m.kk;
     hp.hkk = sc.hk * m.kk;
     hp.h6kk = sc.h6 * m.kk;
+    hp.hn[3] = sc.hk * m.kk;
+    hp.hn[0] = hp.hn[3] / 4.0;
+    hp.hn[1] = hp.hn[3] / 3.0;
+    hp.hn[2] = hp.hn[3] / 2.0;
     const uint64_t planes = w.out_end - w.out_begin;
     // z chunks: enough CTAs to fill the machine, few enough to keep the
     // 8-plane halo overhead per chunk small.

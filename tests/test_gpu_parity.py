@@ -125,6 +125,15 @@ def test_heat_interior_tiles_fast(fast_ctx, g):
     assert_within(pk.mixed_monotonicity(prob, ctx=fast_ctx), oracle_for("mm", prob))
 
 
+def test_heat_fast_mode_long_run(fast_ctx):
+    """100 fast-mode steps on interior tiles: the restructured arithmetic
+    (Horner form of RK4 for the linear field, shared partial sums) stays
+    within the 1e-12 contract over a full-length reach."""
+    m, prob = heat_interior_problem(72, seed=9, steps=100)
+    assert_within(pk.mixed_monotonicity(prob, ctx=fast_ctx), oracle_for("mm", prob))
+    assert_within(pk.growth_bound(prob, ctx=fast_ctx), oracle_for("gb", prob))
+
+
 @pytest.mark.parametrize("variant", ["1x2", "2x2"])
 def test_heat_block_variants(variant):
     """Both heat kernels (1x2 pairs, 2x2 blocks) in both modes: the selector
