@@ -678,7 +678,8 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
-inline bool heat_encode_tmap(CUtensorMap* out, const double* base, uint64_t g, uint64_t planes) {
+inline bool heat_encode_tmap(CUtensorMap* out, const double* base, uint64_t g, uint64_t planes,
+                             cuuint32_t box_x = kHeatXP, cuuint32_t box_y = kHeatW) {
     using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                                 CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
@@ -698,7 +699,7 @@ inline bool heat_encode_tmap(CUtensorMap* out, const double* base, uint64_t g, u
     if ((g * sizeof(double)) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) % 16) != 0) return false;
     const cuuint64_t dims[3] = {g, g, planes};
     const cuuint64_t strides[2] = {g * sizeof(double), g * g * sizeof(double)};
-    const cuuint32_t box[3] = {kHeatXP, kHeatW, 1};
+    const cuuint32_t box[3] = {box_x, box_y, 1};
     const cuuint32_t es[3] = {1, 1, 1};
     // L2 fill granularity of the box loads: a box row is 336 B at a 32 B
     // misalignment, so 64 B fills fetch the least from DRAM (measured, g=800:

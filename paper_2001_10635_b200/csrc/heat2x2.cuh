@@ -17,6 +17,7 @@
 #include <cstdlib>
 
 #include "heat.cuh"
+#include "heat4x4.cuh"
 
 namespace pirk {
 
@@ -569,14 +570,17 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
                              unsigned long long step, unsigned long long* fail,
                              cudaStream_t stream) {
     if (w.out_end <= w.out_begin) return cudaSuccess;
-    // Default: 2x2 blocks in fast mode, 1x2 pairs in exact mode (its longer
-    // per-point expression does not fit 2x2 blocks in registers; measured
-    // faster as pairs).  PIRK_HEAT_BLOCK=1x2|2x2 overrides (A/B comparisons).
-    static const int block2 = [] {
+    // Kernel variant.  Fast mode: 4x4 blocks with TMEM histories (heat4x4.cuh)
+    // whenever the TMA path is available (even g, aligned windows), else 2x2
+    // blocks.  Exact mode: 1x2 pairs (its longer per-point expression does not
+    // fit 2x2 blocks in registers; measured faster as pairs).
+    // PIRK_HEAT_BLOCK=1x2|2x2|4x4 overrides (A/B comparisons; 4x4 is fast-only).
+    static const int variant = [] {
         const char* v = std::getenv("PIRK_HEAT_BLOCK");
         if (v && std::strcmp(v, "1x2") == 0) return 0;
         if (v && std::strcmp(v, "2x2") == 0) return 1;
-        return Exact ? 0 : 1;
+        if (v && std::strcmp(v, "4x4") == 0) return 2;
+        return Exact ? 0 : 2;
     }();
     static bool attr_set = false;
     if (!attr_set) {
@@ -586,9 +590,20 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(heat2_step_kernel<Exact>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kHeatSmemBytes));
+        if constexpr (!Exact) {
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(heat4_step_kernel<Exact>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(k4SmemBytes));
+        }
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
+    static const int n_sm = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 148;
+    }();
     HeatStepParams hp;
     hp.kk = m.kk;
     hp.robin = m.robin;
@@ -600,22 +615,46 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
     hp.hn[1] = hp.hn[3] / 3.0;
     hp.hn[2] = hp.hn[3] / 2.0;
     const uint64_t planes = w.out_end - w.out_begin;
+    const uint64_t wplanes = w.win_end - w.win_begin;
+    const bool vec = (m.g % 2 == 0) && reinterpret_cast<uintptr_t>(w.out0) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(w.out1) % 16 == 0;
+    HeatTmaps tm;
+    std::memset(&tm, 0, sizeof tm);
+    if constexpr (!Exact) {
+        // 16-byte copies need even g and 16-byte aligned windows
+        if (variant == 2 && m.g % 2 == 0 && reinterpret_cast<uintptr_t>(w.in0) % 16 == 0 &&
+            reinterpret_cast<uintptr_t>(w.in1) % 16 == 0) {
+            // z chunks: the count minimising waves x (planes per chunk + 8 halo
+            // planes recomputed per chunk), the wave quantisation of ~tx^2 CTAs
+            const uint64_t tx = (m.g + k4T - 1) / k4T;
+            uint64_t best = 1;
+            double best_cost = 0.0;
+            for (uint64_t c = 1; c <= 8 && c <= planes; ++c) {
+                const uint64_t zc = (planes + c - 1) / c;
+                const uint64_t ctas = tx * tx * 2 * ((planes + zc - 1) / zc);
+                const double cost = static_cast<double>((ctas + n_sm - 1) / n_sm) *
+                                    static_cast<double>(zc + (c > 1 ? 2 * kHeatH : 0));
+                if (c == 1 || cost < best_cost) best = c, best_cost = cost;
+            }
+            const uint64_t zchunk = (planes + best - 1) / best;
+            const uint64_t nchunks = (planes + zchunk - 1) / zchunk;
+            dim3 grid(static_cast<unsigned>(tx), static_cast<unsigned>(tx), static_cast<unsigned>(2 * nchunks));
+            heat4_step_kernel<Exact><<<grid, k4Threads, k4SmemBytes, stream>>>(m, hp, w, sc, step, zchunk, fail,
+                                                                                tm, 1 | (vec ? 2 : 0));
+            return cudaGetLastError();
+        }
+    }
     // z chunks: enough CTAs to fill the machine, few enough to keep the
     // 8-plane halo overhead per chunk small.
     const uint64_t tx = (m.g + kHeatT - 1) / kHeatT;
     uint64_t nchunks = 1;
-    while (tx * tx * 2 * nchunks < 4 * 148 && planes / (nchunks * 2) >= 64) nchunks *= 2;
+    while (tx * tx * 2 * nchunks < 4 * static_cast<uint64_t>(n_sm) && planes / (nchunks * 2) >= 64) nchunks *= 2;
     const uint64_t zchunk = (planes + nchunks - 1) / nchunks;
     nchunks = (planes + zchunk - 1) / zchunk;
     dim3 grid(static_cast<unsigned>(tx), static_cast<unsigned>(tx), static_cast<unsigned>(2 * nchunks));
-    HeatTmaps tm;
-    std::memset(&tm, 0, sizeof tm);
-    const uint64_t wplanes = w.win_end - w.win_begin;
     const int tma = heat_encode_tmap(&tm.f[0], w.in0, m.g, wplanes) &&
                     heat_encode_tmap(&tm.f[1], w.in1, m.g, wplanes);
-    if (block2) {
-        const bool vec = (m.g % 2 == 0) && reinterpret_cast<uintptr_t>(w.out0) % 16 == 0 &&
-                         reinterpret_cast<uintptr_t>(w.out1) % 16 == 0;
+    if (variant >= 1) {
         heat2_step_kernel<Exact><<<grid, kHeat2Threads, kHeatSmemBytes, stream>>>(
             m, hp, w, sc, step, zchunk, fail, tm, tma | (vec ? 2 : 0));
     } else {
