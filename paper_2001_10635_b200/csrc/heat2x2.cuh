@@ -18,6 +18,7 @@
 
 #include "heat.cuh"
 #include "heat4x4.cuh"
+#include "heat_strip.cuh"
 
 namespace pirk {
 
@@ -565,22 +566,40 @@ heat2_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
     if (warp == 0) tmem_dealloc512(tmem_base);
 }
 
+// z-chunk length for one-CTA-per-SM heat kernels over tx x tx tiles and two
+// fields: the count minimising waves x (planes per chunk + 8 halo planes
+// recomputed per chunk), i.e. the wave quantisation of 2 tx^2 CTAs per chunk
+inline uint64_t heat_zchunk(uint64_t tx, uint64_t planes, int n_sm) {
+    uint64_t best = 1;
+    double best_cost = 0.0;
+    for (uint64_t c = 1; c <= 8 && c <= planes; ++c) {
+        const uint64_t zc = (planes + c - 1) / c;
+        const uint64_t ctas = tx * tx * 2 * ((planes + zc - 1) / zc);
+        const double cost = static_cast<double>((ctas + n_sm - 1) / n_sm) *
+                            static_cast<double>(zc + (c > 1 ? 2 * kHeatH : 0));
+        if (c == 1 || cost < best_cost) best = c, best_cost = cost;
+    }
+    return (planes + best - 1) / best;
+}
+
 template <bool Exact>
 cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const StepConsts& sc,
                              unsigned long long step, unsigned long long* fail,
                              cudaStream_t stream) {
     if (w.out_end <= w.out_begin) return cudaSuccess;
-    // Kernel variant.  Fast mode: 4x4 blocks with TMEM histories (heat4x4.cuh)
-    // whenever the TMA path is available (even g, aligned windows), else 2x2
-    // blocks.  Exact mode: 1x2 pairs (its longer per-point expression does not
-    // fit 2x2 blocks in registers; measured faster as pairs).
-    // PIRK_HEAT_BLOCK=1x2|2x2|4x4 overrides (A/B comparisons; 4x4 is fast-only).
+    // Kernel variant.  Fast mode: warp-wide strips with TMEM histories
+    // (heat_strip.cuh) whenever its TMA path is available (even g, aligned
+    // windows), else 2x2 blocks.  Exact mode: 1x2 pairs (its longer per-point
+    // expression does not fit 2x2 blocks in registers; measured faster as pairs).
+    // PIRK_HEAT_BLOCK=1x2|2x2|4x4|strip overrides (A/B comparisons; 4x4 and
+    // strip are fast-only).
     static const int variant = [] {
         const char* v = std::getenv("PIRK_HEAT_BLOCK");
         if (v && std::strcmp(v, "1x2") == 0) return 0;
         if (v && std::strcmp(v, "2x2") == 0) return 1;
         if (v && std::strcmp(v, "4x4") == 0) return 2;
-        return Exact ? 0 : 2;
+        if (v && std::strcmp(v, "strip") == 0) return 3;
+        return Exact ? 0 : 3;
     }();
     static bool attr_set = false;
     if (!attr_set) {
@@ -594,6 +613,9 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
             if (e == cudaSuccess)
                 e = cudaFuncSetAttribute(heat4_step_kernel<Exact>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(k4SmemBytes));
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(heat_strip_kernel<Exact>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSSmemBytes));
         }
         if (e != cudaSuccess) return e;
         attr_set = true;
@@ -621,22 +643,22 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
     HeatTmaps tm;
     std::memset(&tm, 0, sizeof tm);
     if constexpr (!Exact) {
+        if (variant == 3 && heat_encode_tmap(&tm.f[0], w.in0, m.g, wplanes, kSF, kSF) &&
+            heat_encode_tmap(&tm.f[1], w.in1, m.g, wplanes, kSF, kSF)) {
+            const uint64_t tx = (m.g + kST - 1) / kST;
+            const uint64_t zchunk = heat_zchunk(tx, planes, n_sm);
+            const uint64_t nchunks = (planes + zchunk - 1) / zchunk;
+            dim3 grid(static_cast<unsigned>(tx), static_cast<unsigned>(tx), static_cast<unsigned>(2 * nchunks));
+            heat_strip_kernel<Exact><<<grid, kSThreads, kSSmemBytes, stream>>>(m, hp, w, sc, step, zchunk, fail,
+                                                                                tm, 1 | (vec ? 2 : 0));
+            return cudaGetLastError();
+        }
+        std::memset(&tm, 0, sizeof tm);
         // 16-byte copies need even g and 16-byte aligned windows
         if (variant == 2 && m.g % 2 == 0 && reinterpret_cast<uintptr_t>(w.in0) % 16 == 0 &&
             reinterpret_cast<uintptr_t>(w.in1) % 16 == 0) {
-            // z chunks: the count minimising waves x (planes per chunk + 8 halo
-            // planes recomputed per chunk), the wave quantisation of ~tx^2 CTAs
             const uint64_t tx = (m.g + k4T - 1) / k4T;
-            uint64_t best = 1;
-            double best_cost = 0.0;
-            for (uint64_t c = 1; c <= 8 && c <= planes; ++c) {
-                const uint64_t zc = (planes + c - 1) / c;
-                const uint64_t ctas = tx * tx * 2 * ((planes + zc - 1) / zc);
-                const double cost = static_cast<double>((ctas + n_sm - 1) / n_sm) *
-                                    static_cast<double>(zc + (c > 1 ? 2 * kHeatH : 0));
-                if (c == 1 || cost < best_cost) best = c, best_cost = cost;
-            }
-            const uint64_t zchunk = (planes + best - 1) / best;
+            const uint64_t zchunk = heat_zchunk(tx, planes, n_sm);
             const uint64_t nchunks = (planes + zchunk - 1) / zchunk;
             dim3 grid(static_cast<unsigned>(tx), static_cast<unsigned>(tx), static_cast<unsigned>(2 * nchunks));
             heat4_step_kernel<Exact><<<grid, k4Threads, k4SmemBytes, stream>>>(m, hp, w, sc, step, zchunk, fail,

@@ -1,0 +1,459 @@
+// heat_strip.cuh -- K2 v16 (fast mode): the heat3d RK4 step with warp-wide
+// row strips: x-neighbours by shuffle, y-neighbours by one row exchange in
+// shared memory, z-histories in TMEM.
+//
+// Replaces integrate_step (rk4.cpp:30-76) on the heat3d embedding / growth
+// pair exactly as heat.cuh does (models.cpp:92-133; both fields evolve
+// independently under the same linear 7-point operator), held to the fast-mode
+// contract (relative <= 1e-12, never tighter; tests/helpers.assert_within).
+//
+// Why.  heat.cuh / heat2x2.cuh spend ~1.4 shared-memory wavefronts per
+// state-update (67% of the crossbar at g=800, profiles/r01_heat_v14_g800.txt):
+// every stage value is stored and 2-3 neighbours are read back per point.
+// Measured on this B200 (tools/tmem_bw.cu): a 32-bit warp shuffle issues at
+// ~2 per clock per SM, so exchanging a double by shuffle costs a quarter of a
+// shared-memory store + load (4 wavefronts per 32 doubles); tcgen05.ld/st
+// move ~430/360 B/clk/SM, 3x the shared-memory crossbar.
+//
+// Geometry.  A CTA (one per SM) owns a 56x56 x-y tile of one field and streams
+// the planes of a z-chunk; the footprint with the 4-cell halo is 64x64.  Lane l
+// of warp w (16 warps) owns the 2x4 block at footprint columns 2l, 2l+1 and rows
+// 4w .. 4w+3, so a warp spans the whole footprint width: every x-neighbour is
+// in the same thread or the adjacent lane (shfl_up / shfl_down; lanes 0 and 31
+// are halo columns whose garbage never reaches the tile), and every
+// y-neighbour is in the same thread or the same lane of the warp above/below
+// (one double2 row exchanged through shared memory, conflict-free).  Blocks in
+// the 4-cell halo recompute stages 1-3 (the dependency cone); the inner 14x14
+// blocks run stage 4 and store to HBM.  Every thread runs the same code; only
+// the HBM store is predicated.
+//
+// Pipeline.  Iteration j waits for x-plane j (a 64x64 TMA box, zero-filled
+// outside the grid, 4-slot ring, prefetched 2 planes ahead) and evaluates stage
+// 1 at plane j-1, stage 2 at j-2, stage 3 at j-3 and stage 4 at j-4 (the lagged
+// schedule of heat.cuh).  Fast mode evaluates RK4 for this linear autonomous
+// field in Horner form, x + hL(x + hL/2(x + hL/3(x + hL/4 x))): a stage is
+// v_s = x + c_s (sum6(v_{s-1}) - 6 v_{s-1}), c = hk*kk/{4,3,2,1}.  Stage 4's z-
+// and centre terms are folded one iteration early into
+// A4(p) = x(p) + c4 (u3(p-1) - 6 u3(p)).  TMEM holds, per thread, 8 plane slots
+// of its block (16 columns each): x(j-2), x(j-3), u1(j-2), u1(j-3), u2(j-3),
+// u2(j-4), u3(j-4), A4(j-4); x(j-1) and x(j) are read from the x ring.  Each
+// slot a stage overwrites is read (it is the next stage's z- plane) before
+// the stage runs, so every result is stored as soon as it exists.
+//
+// Exchange.  Three levels (u1, u2, u3), each TOP[512] and BOT[512] double2
+// (the first and last row of every block).  Phase A (all four stages) reads the
+// levels published in the previous iteration; after a barrier, phase B
+// publishes this iteration's u1(j-1), u2(j-2), u3(j-3); a second barrier closes
+// the plane.  Stage 1 reads the rows above / below straight from the x ring.
+//
+// Boundaries.  Edge tiles substitute ghost values per point (Robin at x = 0,
+// insulated elsewhere) as heat_pt does; insulated z faces replicate the boundary
+// plane, as heat.cuh.
+#pragma once
+
+#include "heat.cuh"
+#include "tmem_io.cuh"
+
+namespace pirk {
+
+constexpr int kST = 56;                 // output tile edge
+constexpr int kSF = 64;                 // footprint edge
+constexpr int kSThreads = 512;          // 16 warps x 32 lanes, one 2x4 block each
+constexpr int kSXSlots = 4;             // x planes j-1 .. j+2
+constexpr int kSXSlot = kSF * kSF;      // doubles per x slot (row-major, pitch 64)
+constexpr int kSLevel = 2 * kSThreads;  // double2 entries per exchange level: TOP, BOT
+constexpr size_t kSEdgeBytes = size_t(3) * kSLevel * sizeof(double2);          // 48 KB
+constexpr size_t kSRingBytes = size_t(kSXSlots) * kSXSlot * sizeof(double);    // 128 KB
+// [edges][x ring][one row of padding]: the rows above / below the footprint
+// that halo blocks read land in the edge region or the padding
+constexpr size_t kSSmemBytes = kSEdgeBytes + kSRingBytes + kSF * sizeof(double);
+
+// TMEM plane slots of a thread (16 columns = 8 doubles each)
+enum : int { kSX = 0, kSU1 = 2, kSU2 = 4, kSU3 = 6, kSA4 = 7 };
+
+// Non-finite output at plane p (cold path): read the block's stored cells back
+// and record each bad one (atomicMin keeps the lowest component).
+__device__ __forceinline__ void heat_strip_report(const double* stp, int g, long long g2, int p, int gout,
+                                                  unsigned mask, int field, int method,
+                                                  unsigned long long step, unsigned long long* fail,
+                                                  unsigned long long n_total) {
+#pragma unroll 1
+    for (int i = 0; i < 8; ++i) {
+        const int r = i >> 1, c = i & 1;
+        if (!((mask >> i) & 1)) continue;
+        if (finite_d(stp[r * g + c])) continue;
+        const unsigned long long gi =
+            static_cast<unsigned long long>(static_cast<long long>(p) * g2 + gout + r * g + c);
+        if (method == 0)
+            record_fail(fail, step, gi + (field ? n_total : 0ull));
+        else if (fail)
+            record_fail(fail + field, step, gi);
+    }
+}
+
+template <bool Interior>
+struct HeatStrip {
+    const HeatStepParams& hp;
+    double2* __restrict__ EX;  // exchange levels
+    double* __restrict__ XR;   // x ring
+    int t;                     // thread = block index (warp * 32 + lane)
+    int xo;                    // own block offset in an x slot: row 4w, column 2l
+    int zs, ze, ob, oe, g, lo_shift, hi_shift;
+    long long g2;
+    double* __restrict__ stp;  // output plane j-4 at the own block's (0,0)
+    bool st_own;               // own block with all 8 cells in the grid (vector stores)
+    unsigned st_mask;          // edge tiles: per-cell store mask (bit 2r+c)
+    int gout;                  // in-plane global offset of the block's (0,0) cell
+    int fx0, fxg, fy0, fyg;    // edge tiles: columns at x=0 / x=g-1 (2 bits), rows at y=0 / y=g-1 (4 bits)
+    int field, method;
+    unsigned long long step;
+    unsigned long long* fail;
+    unsigned long long n_total;
+    const void* tmap;
+    int bx0, by0, wbz;
+    unsigned long long* bars;
+    unsigned tt;  // TMEM address of slot 0
+    int xs;       // x ring slot of plane j
+    int xph;      // mbarrier phase bit per slot
+
+    __device__ __forceinline__ unsigned ts(int slot) const { return tt + 16u * slot; }
+    __device__ __forceinline__ double* xslot(int s) const { return XR + s * kSXSlot; }
+
+    __device__ __forceinline__ void tma(int p, int s) {
+        mbar_expect_tx(bars + s, kSXSlot * sizeof(double));
+        tma_load_plane(xslot(s), tmap, bx0, by0, p - wbz, bars + s);
+    }
+
+    // own 2x4 block of an x slot (v[2r + c])
+    __device__ __forceinline__ void own_x(const double* X, double (&v)[8]) const {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const double2 a = *reinterpret_cast<const double2*>(X + xo + r * kSF);
+            v[2 * r] = a.x;
+            v[2 * r + 1] = a.y;
+        }
+    }
+
+    // rows above / below the block: from the x slot (stage 1) or a level
+    __device__ __forceinline__ void x_tb(const double* X, double (&T)[2], double (&B)[2]) const {
+        const double2 a = *reinterpret_cast<const double2*>(X + xo - kSF);
+        const double2 c = *reinterpret_cast<const double2*>(X + xo + 4 * kSF);
+        T[0] = a.x, T[1] = a.y, B[0] = c.x, B[1] = c.y;
+    }
+    __device__ __forceinline__ void u_tb(int level, double (&T)[2], double (&B)[2]) const {
+        const double2* L = EX + level * kSLevel;
+        const double2 a = L[kSThreads + t - 32];  // BOT of the block above
+        const double2 c = L[t + 32];              // TOP of the block below
+        T[0] = a.x, T[1] = a.y, B[0] = c.x, B[1] = c.y;
+    }
+    __device__ __forceinline__ void publish(int level, const double (&v)[8]) const {
+        double2* L = EX + level * kSLevel;
+        L[t] = make_double2(v[0], v[1]);
+        L[kSThreads + t] = make_double2(v[6], v[7]);
+    }
+
+    // in-plane sums xm + xp + ym + yp of the 8 points of centre plane C
+    __device__ __forceinline__ void inplane(const double (&C)[8], const double (&T)[2], const double (&B)[2],
+                                            double (&s)[8]) const {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const double L = __shfl_up_sync(0xffffffffu, C[2 * r + 1], 1);
+            const double R = __shfl_down_sync(0xffffffffu, C[2 * r], 1);
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const double ctr = C[2 * r + c];
+                double xm = c ? C[2 * r] : L;
+                double xp = c ? R : C[2 * r + 1];
+                double ym = r > 0 ? C[2 * (r - 1) + c] : T[c];
+                double yp = r < 3 ? C[2 * (r + 1) + c] : B[c];
+                if constexpr (!Interior) {
+                    xm = ((fx0 >> c) & 1) ? fma(-hp.robin, ctr, xp) : xm;
+                    xp = ((fxg >> c) & 1) ? ctr : xp;
+                    ym = ((fy0 >> r) & 1) ? ctr : ym;
+                    yp = ((fyg >> r) & 1) ? ctr : yp;
+                }
+                s[2 * r + c] = (xm + xp) + (ym + yp);
+            }
+        }
+    }
+
+    // o = base + cs (inplane + zm + zp - 6 C)
+    __device__ __forceinline__ void stage(const double (&C)[8], const double (&T)[2], const double (&B)[2],
+                                          const double (&zm)[8], const double (&zp)[8], const double (&bs)[8],
+                                          double cs, double (&o)[8]) const {
+        double s[8];
+        inplane(C, T, B, s);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = fma(cs, fma(-6.0, C[i], s[i] + (zm[i] + zp[i])), bs[i]);
+    }
+
+    // One plane of the pipeline.  edge: the iteration touches a chunk edge or
+    // an insulated z face (validity and face tests, uniform branches).
+    template <int PH>
+    __device__ __forceinline__ void iteration(int j, bool edge) {
+        // x(q) in TMEM slot kSX + (q & 1); u1(q) in kSU1 + (q & 1); u2(q) in kSU2 + (q & 1)
+        constexpr int XA = kSX + PH, XB = kSX + (PH ^ 1);      // x(j-2), x(j-3)
+        constexpr int U1A = kSU1 + PH, U1B = kSU1 + (PH ^ 1);  // u1(j-2), u1(j-3)
+        constexpr int U2A = kSU2 + (PH ^ 1), U2B = kSU2 + PH;  // u2(j-3), u2(j-4)
+        const bool v1 = !edge || (j - 1 >= zs + lo_shift && j - 1 < ze - hi_shift);
+        const bool v2 = !edge || (j - 2 >= zs + 2 * lo_shift && j - 2 < ze - 2 * hi_shift);
+        const bool v3 = !edge || (j - 3 >= zs + 3 * lo_shift && j - 3 < ze - 3 * hi_shift);
+        const bool v4 = !edge || (j - 4 >= ob && j - 4 < oe);
+        const bool a4 = !edge || (v3 && j - 3 >= ob && j - 3 < oe);  // A4(j-3) needed next iteration
+        const bool has_x = !edge || j < ze;
+
+        // ---- x(j): wait for its box; prefetch x(j+2) into the slot of x(j-2)
+        const double* Xj = xslot(xs);
+        const double* Xm = xslot((xs + 3) & 3);  // x(j-1)
+        if (has_x) {
+            mbar_wait(bars + xs, (xph >> xs) & 1);
+            if (threadIdx.x == 0 && (!edge || j + 2 < ze)) tma(j + 2, (xs + 2) & 3);
+        }
+
+        // ---- stage 1 at p = j-1: centre and base x(j-1), z- x(j-2), z+ x(j)
+        double o1[8], zm2[8];
+        if (v1) {
+            double C[8], zm[8], zp[8], T[2], B[2];
+            own_x(Xm, C);
+            tm_ld8x2(ts(XA), ts(U1B), zm, zm2);  // x(j-2); u1(j-3) before it is overwritten
+            if (!edge || j < g) {
+                own_x(Xj, zp);
+            } else {  // x(g) := x(g-1)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) zp[i] = C[i];
+            }
+            if (edge && j - 1 == 0) {  // x(-1) := x(0)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) zm[i] = C[i];
+            }
+            x_tb(Xm, T, B);
+            stage(C, T, B, zm, zp, C, hp.hn[0], o1);
+            tm_st8(ts(U1B), o1);  // u1(j-1) replaces u1(j-3)
+        } else if (v2) {
+            tm_ld8(ts(U1B), zm2);
+        }
+        // ---- stage 2 at p = j-2: centre u1(j-2), z- u1(j-3), z+ u1(j-1), base x(j-2)
+        double o2[8], zm3[8];
+        if (v2) {
+            double C[8], bs[8], T[2], B[2];
+            tm_ld8x2(ts(U1A), ts(XA), C, bs);
+            tm_ld8(ts(U2B), zm3);  // u2(j-4) before it is overwritten
+            if (edge && j - 2 == 0) {  // u1(-1) := u1(0)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) zm2[i] = C[i];
+            }
+            if (edge && j - 2 == g - 1) {  // u1(g) := u1(g-1)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) o1[i] = C[i];
+            }
+            u_tb(0, T, B);
+            stage(C, T, B, zm2, o1, bs, hp.hn[1], o2);
+            tm_st8(ts(U2B), o2);  // u2(j-2) replaces u2(j-4)
+        } else if (v3) {
+            tm_ld8(ts(U2B), zm3);
+        }
+        // ---- stage 3 at p = j-3: centre u2(j-3), z- u2(j-4), z+ u2(j-2), base x(j-3)
+        double o3[8], C4[8];
+        if (v4 || a4) tm_ld8(ts(kSU3), C4);  // u3(j-4) before it is overwritten
+        if (v3) {
+            double C[8], bs[8], T[2], B[2];
+            tm_ld8x2(ts(U2A), ts(XB), C, bs);
+            if (edge && j - 3 == 0) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) zm3[i] = C[i];
+            }
+            if (edge && j - 3 == g - 1) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) o2[i] = C[i];
+            }
+            u_tb(1, T, B);
+            stage(C, T, B, zm3, o2, bs, hp.hn[2], o3);
+            tm_st8(ts(kSU3), o3);  // u3(j-3) replaces u3(j-4)
+        }
+        // ---- stage 4 at p = j-4: y = A4(j-4) + c4 (inplane(u3(j-4)) + u3(j-3)) to
+        // HBM; A4(j-3) = x(j-3) + c4 (u3(j-4) - 6 u3(j-3)); x(j-1) replaces x(j-3)
+        {
+            double av[8], x3[8];
+            tm_ld8x2(ts(kSA4), ts(XB), av, x3);
+            if (edge && j - 4 == g - 1) {  // u3(g) := u3(g-1) (stage 3 did not run)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) o3[i] = C4[i];
+            }
+            if (edge && j - 3 == 0) {  // u3(-1) := u3(0) (stage 4 does not run)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) C4[i] = o3[i];
+            }
+            if (v4) {
+                double T[2], B[2], s[8], y[8];
+                u_tb(2, T, B);
+                inplane(C4, T, B, s);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) y[i] = fma(hp.hn[3], s[i] + o3[i], av[i]);
+                if (st_own) {
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        *reinterpret_cast<double2*>(stp + r * g) = make_double2(y[2 * r], y[2 * r + 1]);
+                } else if (st_mask) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        if ((st_mask >> i) & 1) stp[(i >> 1) * g + (i & 1)] = y[i];
+                }
+                if ((st_own || st_mask) &&
+                    !finite_d(((y[0] + y[1]) + (y[2] + y[3])) + ((y[4] + y[5]) + (y[6] + y[7]))))
+                    heat_strip_report(stp, g, g2, j - 4, gout, st_own ? 0xffu : st_mask, field, method, step,
+                                      fail, n_total);
+            }
+            if (a4) {
+                double an[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) an[i] = fma(hp.hn[3], fma(-6.0, o3[i], C4[i]), x3[i]);
+                tm_st8(ts(kSA4), an);
+            }
+            double w[8];
+            own_x(Xm, w);
+            tm_st8(ts(XB), w);  // x(j-1) replaces x(j-3)
+        }
+        if (has_x) {
+            xph ^= 1 << xs;
+            xs = (xs + 1) & 3;
+        }
+        __syncthreads();  // phase A's exchange reads are complete
+        // ---- phase B: publish the first / last rows of u1(j-1), u2(j-2), u3(j-3)
+        if (v1) publish(0, o1);
+        if (v2) publish(1, o2);
+        if (v3) publish(2, o3);
+        stp += g2;
+        __syncthreads();
+    }
+
+    __device__ __forceinline__ void one(int j, bool edge) {
+        if (j & 1)
+            iteration<1>(j, edge);
+        else
+            iteration<0>(j, edge);
+    }
+
+    __device__ __forceinline__ void run() {
+        xs = 0;
+        xph = 0;
+        if (threadIdx.x == 0) {
+            if (zs < ze) tma(zs, 0);
+            if (zs + 1 < ze) tma(zs + 1, 1);
+        }
+        const int jend = ze + 4;
+        // steady state: all stages valid, planes j-5 .. j clear of the z faces
+        // (heat.cuh's bounds) and x(j+2) inside the window
+        int a = zs + 3 + 3 * lo_shift;
+        if (a < ob + 4) a = ob + 4;
+        if (a < 5) a = 5;
+        int bnd = ze - 2;
+        if (bnd > oe + 4) bnd = oe + 4;
+        if (bnd > g) bnd = g;
+        if (bnd < a) bnd = a;
+        int j = zs;
+        for (; j < a && j < jend; ++j) one(j, true);
+        if ((j & 1) && j < bnd) iteration<1>(j++, false);
+        for (; j + 1 < bnd; j += 2) {
+            iteration<0>(j, false);
+            iteration<1>(j + 1, false);
+        }
+        for (; j < jend; ++j) one(j, j >= bnd);
+    }
+};
+
+template <bool Exact>
+__global__ void __launch_bounds__(kSThreads, 1)
+heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w, const StepConsts sc,
+                  const unsigned long long step, const uint64_t zchunk,
+                  unsigned long long* __restrict__ fail, const __grid_constant__ HeatTmaps tm, const int flags) {
+    static_assert(!Exact, "heat_strip_kernel is the fast-mode kernel");
+    (void)sizeof(ModeCheck<Exact>);
+    (void)sc;
+    extern __shared__ __align__(128) double smem[];
+    __shared__ __align__(8) unsigned long long bars[kSXSlots];
+    __shared__ unsigned tmem_base;
+    const int tid = threadIdx.x;
+    const long long g = static_cast<long long>(m.g);
+    const int field = blockIdx.z & 1;
+    const long long chunk = blockIdx.z >> 1;
+    const long long ix0 = static_cast<long long>(blockIdx.x) * kST;
+    const long long iy0 = static_cast<long long>(blockIdx.y) * kST;
+    const long long obz = static_cast<long long>(w.out_begin) + chunk * static_cast<long long>(zchunk);
+    long long oez = obz + static_cast<long long>(zchunk);
+    if (oez > static_cast<long long>(w.out_end)) oez = static_cast<long long>(w.out_end);
+    if (obz >= oez) return;
+
+    const int warp = tid >> 5, lane = tid & 31;
+    const long long gx0 = ix0 - kHeatH + 2 * lane, gy0 = iy0 - kHeatH + 4 * warp;
+    const bool own = lane >= 2 && lane <= 29 && warp >= 1 && warp <= 14;
+    const bool interior = ix0 - kHeatH >= 0 && ix0 + kST + kHeatH <= g && iy0 - kHeatH >= 0 &&
+                          iy0 + kST + kHeatH <= g;
+    unsigned st_mask = 0;
+    int fx0 = 0, fxg = 0, fy0 = 0, fyg = 0;
+    for (int c = 0; c < 2; ++c) {
+        fx0 |= (gx0 + c == 0) << c;
+        fxg |= (gx0 + c == g - 1) << c;
+    }
+    for (int r = 0; r < 4; ++r) {
+        fy0 |= (gy0 + r == 0) << r;
+        fyg |= (gy0 + r == g - 1) << r;
+    }
+    if (own) {
+        for (int i = 0; i < 8; ++i) {
+            const long long x = gx0 + (i & 1), y = gy0 + (i >> 1);
+            if (x >= 0 && x < g && y >= 0 && y < g) st_mask |= 1u << i;
+        }
+    }
+    const bool st_own = own && st_mask == 0xffu && (flags & 2);
+    if (st_own) st_mask = 0;  // vector path
+    const int gout = (gx0 >= 0 && gy0 >= 0) ? static_cast<int>(gy0 * g + gx0) : 0;
+
+    const long long g2 = g * g;
+    const int zs = static_cast<int>((obz - kHeatH > 0) ? obz - kHeatH : 0);
+    const int ze = static_cast<int>((oez + kHeatH < g) ? oez + kHeatH : g);
+    double* dst = (field ? w.out1 : w.out0) - static_cast<long long>(w.out_begin) * g2;
+
+    if (warp == 0) tmem_alloc512(&tmem_base);
+    if (tid == 0) {
+        for (int s = 0; s < kSXSlots; ++s) mbar_init(bars + s, 1);
+        mbar_fence_init();
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    // warp w: TMEM lane quadrant w % 4, columns 128 (w / 4) .. +127 (8 slots of 16)
+    const unsigned tt = tmem_base + (static_cast<unsigned>(32 * (warp & 3)) << 16) +
+                        static_cast<unsigned>(128 * (warp >> 2));
+#define PIRK_STRIP_RUN(INTERIOR)                                                                     \
+    {                                                                                                \
+        HeatStrip<INTERIOR> r{hp};                                                                   \
+        r.EX = reinterpret_cast<double2*>(smem);                                                     \
+        r.XR = smem + kSEdgeBytes / sizeof(double);                                                  \
+        r.t = tid;                                                                                   \
+        r.xo = 4 * warp * kSF + 2 * lane;                                                            \
+        r.zs = zs, r.ze = ze, r.ob = static_cast<int>(obz), r.oe = static_cast<int>(oez);           \
+        r.g = static_cast<int>(g), r.lo_shift = zs > 0, r.hi_shift = ze < g;                         \
+        r.g2 = g2;                                                                                   \
+        r.gout = gout;                                                                               \
+        r.stp = dst + static_cast<long long>(zs - 4) * g2 + gout;                                    \
+        r.st_own = st_own, r.st_mask = st_mask;                                                      \
+        r.fx0 = fx0, r.fxg = fxg, r.fy0 = fy0, r.fyg = fyg;                                          \
+        r.field = field, r.method = m.method, r.step = step, r.fail = fail;                          \
+        r.n_total = static_cast<unsigned long long>(g2 * g);                                         \
+        r.tmap = &tm.f[field];                                                                       \
+        r.bx0 = static_cast<int>(ix0) - kHeatH, r.by0 = static_cast<int>(iy0) - kHeatH;              \
+        r.wbz = static_cast<int>(w.win_begin);                                                       \
+        r.bars = bars;                                                                               \
+        r.tt = tt;                                                                                   \
+        r.run();                                                                                     \
+    }
+    if (interior) PIRK_STRIP_RUN(true) else PIRK_STRIP_RUN(false)
+#undef PIRK_STRIP_RUN
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc512(tmem_base);
+}
+
+}  // namespace pirk
