@@ -12,6 +12,8 @@ import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libpirk_b200.so")
+# development A/B builds only (tools/ab_build.py): load another build of the same ABI
+LIB_PATH = os.environ.get("PIRK_LIB", LIB_PATH)
 HEADER = os.path.join(HERE, "..", "include", "pirk_c.h")
 
 # pirk_status

@@ -40,17 +40,21 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(s) <= t for s in _sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Compile the three translation units and link `out`.  `defines` (extra
+    -D flags) and `out` exist for development A/B builds (tools/ab_build.py)."""
+    if not force and out == LIB and up_to_date():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(LIBDIR, "obj")
+    libdir = os.path.dirname(out)
+    os.makedirs(libdir, exist_ok=True)
+    objdir = os.path.join(libdir, "obj" if out == LIB else "obj_" + os.path.basename(out))
     os.makedirs(objdir, exist_ok=True)
 
     def compile_one(item):
         src, flags = item
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *COMMON, *flags, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *ARCH, *COMMON, *flags, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src),
+               "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -64,14 +68,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for _, log in results:
             sys.stderr.write(log)
     objs = [o for o, _ in results]
-    tmp = LIB + ".tmp"
+    tmp = out + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-ccbin", "/usr/bin/g++", *objs,
            "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
