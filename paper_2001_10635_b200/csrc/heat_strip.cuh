@@ -41,10 +41,11 @@
 // the stage runs, so every result is stored as soon as it exists.
 //
 // Exchange.  Three levels (u1, u2, u3), each TOP[512] and BOT[512] double2
-// (the first and last row of every block).  Phase A (all four stages) reads the
-// levels published in the previous iteration; after a barrier, phase B
-// publishes this iteration's u1(j-1), u2(j-2), u3(j-3); a second barrier closes
-// the plane.  Stage 1 reads the rows above / below straight from the x ring.
+// (the first and last row of every block), double-buffered by iteration
+// parity: a stage reads the rows its predecessor published in the previous
+// iteration and publishes its own rows as soon as they exist, so one barrier
+// per plane suffices.  Stage 1 reads the rows above / below straight from the
+// x ring.
 //
 // Boundaries.  Edge tiles substitute ghost values per point (Robin at x = 0,
 // insulated elsewhere) as heat_pt does; insulated z faces replicate the boundary
@@ -69,10 +70,10 @@ constexpr int kSThreads = 512;          // 16 warps x 32 lanes, one 2x4 block ea
 constexpr int kSXSlots = 4;             // x planes j-1 .. j+2
 constexpr int kSXSlot = kSF * kSF;      // doubles per x slot (row-major, pitch 64)
 constexpr int kSLevel = 2 * kSThreads;  // double2 entries per exchange level: TOP, BOT
-constexpr size_t kSEdgeBytes = size_t(3) * kSLevel * sizeof(double2);          // 48 KB
+constexpr size_t kSEdgeBytes = size_t(2 * 3) * kSLevel * sizeof(double2);      // 96 KB: 2 buffers x 3 levels
 constexpr size_t kSRingBytes = size_t(kSXSlots) * kSXSlot * sizeof(double);    // 128 KB
-// [edges][x ring][one row of padding]: the rows above / below the footprint
-// that halo blocks read land in the edge region or the padding
+// [exchange][x ring][one row of padding]: the rows above / below the
+// footprint that halo blocks read land in the exchange region or the padding
 constexpr size_t kSSmemBytes = kSEdgeBytes + kSRingBytes + kSF * sizeof(double);
 
 // TMEM plane slots of a thread (16 columns = 8 doubles each)
@@ -148,14 +149,15 @@ struct HeatStrip {
         const double2 c = *reinterpret_cast<const double2*>(X + xo + 4 * kSF);
         T[0] = a.x, T[1] = a.y, B[0] = c.x, B[1] = c.y;
     }
-    __device__ __forceinline__ void u_tb(int level, double (&T)[2], double (&B)[2]) const {
-        const double2* L = EX + level * kSLevel;
+    // exchange buffer `buf` (iteration parity) of level 0..2 (u1..u3)
+    __device__ __forceinline__ void u_tb(int buf, int level, double (&T)[2], double (&B)[2]) const {
+        const double2* L = EX + (3 * buf + level) * kSLevel;
         const double2 a = L[kSThreads + t - 32];  // BOT of the block above
         const double2 c = L[t + 32];              // TOP of the block below
         T[0] = a.x, T[1] = a.y, B[0] = c.x, B[1] = c.y;
     }
-    __device__ __forceinline__ void publish(int level, const double (&v)[8]) const {
-        double2* L = EX + level * kSLevel;
+    __device__ __forceinline__ void publish(int buf, int level, const double (&v)[8]) const {
+        double2* L = EX + (3 * buf + level) * kSLevel;
         L[t] = make_double2(v[0], v[1]);
         L[kSThreads + t] = make_double2(v[6], v[7]);
     }
@@ -264,6 +266,7 @@ struct HeatStrip {
             x_tb(Xm, T, B);
             stage(C, T, B, zm, zp, C, hp.hn[0], o1);
             tm_st8(ts(U1B), o1);  // u1(j-1) replaces u1(j-3)
+            publish(PH, 0, o1);
         } else if (v2) {
             tm_ld8(ts(U1B), zm2);
         }
@@ -281,9 +284,10 @@ struct HeatStrip {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) o1[i] = C[i];
             }
-            u_tb(0, T, B);
+            u_tb(PH ^ 1, 0, T, B);
             stage(C, T, B, zm2, o1, bs, hp.hn[1], o2);
             tm_st8(ts(U2B), o2);  // u2(j-2) replaces u2(j-4)
+            publish(PH, 1, o2);
         } else if (v3) {
             tm_ld8(ts(U2B), zm3);
         }
@@ -302,9 +306,10 @@ struct HeatStrip {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) o2[i] = C[i];
             }
-            u_tb(1, T, B);
+            u_tb(PH ^ 1, 1, T, B);
             stage(C, T, B, zm3, o2, bs, hp.hn[2], o3);
             if (inner) tm_st8(ts(kSU3), o3);  // u3(j-3) replaces u3(j-4)
+            publish(PH, 2, o3);
         }
         // ---- stage 4 at p = j-4: y = A4(j-4) + c4 (inplane(u3(j-4)) + u3(j-3)) to
         // HBM; A4(j-3) = x(j-3) + c4 (u3(j-4) - 6 u3(j-3)); x(j-1) replaces x(j-3)
@@ -321,7 +326,7 @@ struct HeatStrip {
             }
             if (v4) {
                 double T[2], B[2], s[8], y[8];  // (halo lanes compute garbage, store nothing)
-                u_tb(2, T, B);
+                u_tb(PH ^ 1, 2, T, B);
                 inplane(C4, T, B, s);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) y[i] = fma(hp.hn[3], s[i] + o3[i], av[i]);
@@ -355,12 +360,9 @@ struct HeatStrip {
             xph ^= 1 << xs;
             xs = (xs + 1) & 3;
         }
-        __syncthreads();  // phase A's exchange reads are complete
-        // ---- phase B: publish the first / last rows of u1(j-1), u2(j-2), u3(j-3)
-        if (v1) publish(0, o1);
-        if (v2) publish(1, o2);
-        if (v3) publish(2, o3);
         stp += g2;
+        // one barrier per plane: this iteration's rows (buffer j & 1) become
+        // readable, and the next iteration may overwrite buffer (j - 1) & 1
         __syncthreads();
     }
 
