@@ -128,6 +128,20 @@ struct HeatStrip {
     __device__ __forceinline__ unsigned ts(int slot) const { return tt + 16u * slot; }
     __device__ __forceinline__ double* xslot(int s) const { return XR + s * kSXSlot; }
 
+#ifndef PIRK_STRIP_ST2
+#define PIRK_STRIP_ST2 1
+#endif
+    // Store a plane slot.  One 2-column store per double: an x16 store needs its
+    // 16 source registers contiguous, which costs ~16 register moves per store.
+    __device__ __forceinline__ void st8(unsigned ta, const double (&v)[8]) const {
+        if constexpr (PIRK_STRIP_ST2) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) tm_st1(ta + 2 * i, v[i]);
+        } else {
+            tm_st8(ta, v);
+        }
+    }
+
     __device__ __forceinline__ void tma(int p, int s) {
         mbar_expect_tx(bars + s, kSXSlot * sizeof(double));
         tma_load_plane(xslot(s), tmap, bx0, by0, p - wbz, bars + s);
@@ -265,7 +279,7 @@ struct HeatStrip {
             }
             x_tb(Xm, T, B);
             stage(C, T, B, zm, zp, C, hp.hn[0], o1);
-            tm_st8(ts(U1B), o1);  // u1(j-1) replaces u1(j-3)
+            st8(ts(U1B), o1);  // u1(j-1) replaces u1(j-3)
             publish(PH, 0, o1);
         } else if (v2) {
             tm_ld8(ts(U1B), zm2);
@@ -286,7 +300,7 @@ struct HeatStrip {
             }
             u_tb(PH ^ 1, 0, T, B);
             stage(C, T, B, zm2, o1, bs, hp.hn[1], o2);
-            tm_st8(ts(U2B), o2);  // u2(j-2) replaces u2(j-4)
+            st8(ts(U2B), o2);  // u2(j-2) replaces u2(j-4)
             publish(PH, 1, o2);
         } else if (v3) {
             tm_ld8(ts(U2B), zm3);
@@ -308,7 +322,7 @@ struct HeatStrip {
             }
             u_tb(PH ^ 1, 1, T, B);
             stage(C, T, B, zm3, o2, bs, hp.hn[2], o3);
-            if (inner) tm_st8(ts(kSU3), o3);  // u3(j-3) replaces u3(j-4)
+            if (inner) st8(ts(kSU3), o3);  // u3(j-3) replaces u3(j-4)
             publish(PH, 2, o3);
         }
         // ---- stage 4 at p = j-4: y = A4(j-4) + c4 (inplane(u3(j-4)) + u3(j-3)) to
@@ -348,13 +362,13 @@ struct HeatStrip {
                 double an[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) an[i] = fma(hp.hn[3], fma(-6.0, o3[i], C4[i]), x3[i]);
-                tm_st8(ts(kSA4), an);
+                st8(ts(kSA4), an);
             }
         }
         {
             double w[8];
             own_x(Xm, w);
-            tm_st8(ts(XB), w);  // x(j-1) replaces x(j-3)
+            st8(ts(XB), w);  // x(j-1) replaces x(j-3)
         }
         if (has_x) {
             xph ^= 1 << xs;
