@@ -105,6 +105,18 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def heat_kernel_name(mode, grid):
+    """The heat kernel launch_heat_step (csrc/heat2x2.cuh) runs for this mode and
+    grid: warp-wide strips in fast mode (TMA path: even g), 1x2 pairs in exact
+    mode; PIRK_HEAT_BLOCK=1x2|2x2|4x4|strip overrides."""
+    v = os.environ.get("PIRK_HEAT_BLOCK", "")
+    if mode == "fast" and grid % 2 == 0 and v in ("", "strip", "4x4"):
+        return "heat4_step_kernel" if v == "4x4" else "heat_strip_kernel"
+    if v == "1x2" or (v == "" and mode != "fast"):
+        return "heat_step_kernel"
+    return "heat2_step_kernel"
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -308,8 +320,7 @@ def run_ours(args):
     launch_bytes = 16.0 * 2 * n / world
     achieved = launch_bytes / (per_launch_ms * 1e-3) / 1e9
     traffic = None
-    # dominant kernel by mode (heat2x2.cuh launch_heat_step): 2x2 blocks in fast mode
-    kernel = "heat2_step_kernel" if args.mode == "fast" else "heat_step_kernel"
+    kernel = heat_kernel_name(args.mode, args.grid)
     tp = os.path.join(ROOT, "profiles", "heat_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:

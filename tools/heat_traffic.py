@@ -20,7 +20,7 @@ for mode in ("fast", "exact"):
            os.path.join(ROOT, "tools", "prof_target.py"), "heat", str(grid), mode, "2"]
     r = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT)
     txt = r.stdout + r.stderr
-    kern = re.search(r"void (heat\w*_step_kernel)<", txt)
+    kern = re.search(r"void (heat\w*kernel)<", txt)
 
     def metric(name):
         m = re.search(name + r"\s+(\w+)\s+([\d.,]+)", txt)
