@@ -476,8 +476,10 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
     __syncthreads();
     tmem_fence_after();
     // warp w: TMEM lane quadrant w % 4, columns 128 (w / 4) .. +127 (8 slots of 16)
-    const unsigned tt = tmem_base + (static_cast<unsigned>(32 * (warp & 3)) << 16) +
-                        static_cast<unsigned>(128 * (warp >> 2));
+    // (through a warp reduction: its result lives in a uniform register, so the
+    // TMEM addresses of the loop's tcgen05 ops need no per-use R2UR)
+    const unsigned tt = __reduce_or_sync(0xffffffffu, tmem_base + (static_cast<unsigned>(32 * (warp & 3)) << 16) +
+                                                          static_cast<unsigned>(128 * (warp >> 2)));
 #define PIRK_STRIP_RUN(INTERIOR)                                                                     \
     {                                                                                                \
         HeatStrip<INTERIOR> r{hp};                                                                   \
