@@ -148,6 +148,20 @@ def test_heat_block_variants(variant):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("variant", ["smem", "warp"])
+def test_chain_kernel_variants(variant):
+    """Both chain kernels in both modes (defaults: warp-tiled in fast mode,
+    shared-memory tiles in exact mode) on the traffic and coupled-chain tests."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PIRK_CHAIN_KERNEL=variant)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        os.path.join(root, "tests", "test_gpu_parity.py"),
+                        "-k", "(traffic or chain) and not variant"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 # -------------------------------------------------------------------- chain
 
 @pytest.mark.parametrize("n", [1, 2, 7, 1000, 1016, 1017, 5000])
