@@ -25,11 +25,21 @@ def run(name, prob, mode, steps):
     eng.close(); ctx.close()
 
 g = int(sys.argv[1]) if len(sys.argv) > 1 else 400
-for mode in ("exact", "fast"):
-    m = pk.make_heat3d(g)
-    n = g ** 3
-    prob = pk.ReachProblem(m, pk.IntervalVector(np.full(n, 0.9), np.full(n, 1.1)), None, 0.0, 100 * 5e-8, 5e-8, 0)
-    run(f"heat3d g={g}", prob, mode, 20)
+# PROBE_MODES=fast|exact|exact,fast; PROBE=heat|chain|all (default all)
+modes = os.environ.get("PROBE_MODES", "exact,fast").split(",")
+what = os.environ.get("PROBE", "all")
+for mode in modes:
+    if what in ("all", "heat"):
+        m = pk.make_heat3d(g)
+        n = g ** 3
+        prob = pk.ReachProblem(m, pk.IntervalVector(np.full(n, 0.9), np.full(n, 1.1)), None, 0.0, 100 * 5e-8, 5e-8, 0)
+        run(f"heat3d g={g}", prob, mode, 20)
+    if what == "heat":
+        continue
+    n6 = 10**6
+    m = pk.make_traffic(n6)
+    prob = pk.ReachProblem(m, pk.IntervalVector(np.full(n6, 10.0), np.full(n6, 20.0)), pk.IntervalVector([4.0], [6.0]), 0.0, 30.0, 0.5, 0)
+    run("traffic n=1e6", prob, mode, 60)
     m = pk.make_traffic(10**7)
     prob = pk.ReachProblem(m, pk.IntervalVector(np.full(10**7, 10.0), np.full(10**7, 20.0)), pk.IntervalVector([4.0], [6.0]), 0.0, 30.0, 0.5, 0)
     run("traffic n=1e7", prob, mode, 20)
