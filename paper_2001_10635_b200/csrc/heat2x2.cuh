@@ -570,6 +570,11 @@ heat2_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
 // fields: the count minimising waves x (planes per chunk + 8 halo planes
 // recomputed per chunk), i.e. the wave quantisation of 2 tx^2 CTAs per chunk
 inline uint64_t heat_zchunk(uint64_t tx, uint64_t planes, int n_sm) {
+    static const int forced = [] {  // PIRK_HEAT_ZCHUNKS=c forces c chunks (A/B only)
+        const char* v = std::getenv("PIRK_HEAT_ZCHUNKS");
+        return v ? std::atoi(v) : 0;
+    }();
+    if (forced > 0) return (planes + forced - 1) / forced;
     uint64_t best = 1;
     double best_cost = 0.0;
     for (uint64_t c = 1; c <= 8 && c <= planes; ++c) {
