@@ -407,3 +407,40 @@ def test_cuda_matches_reference_golden(ctx, case):
         assert_within(tube, R, rel=1e-12, atol=1e-14, never_tighter=(method != O.METHOD_MC))
     else:
         assert_bitexact(tube, R)
+
+
+# ------------------------------------------------------------ formats / driver
+
+def test_tube_formats_match_reference_io(ctx):
+    """The CUDA tube of traffic n=5 through tube_to_csv / tube_to_json is
+    byte-identical to the reference's io.cpp output (tests/golden/io, written by
+    oracle/ref_io_golden.cpp); only the report's wall-clock phases differ and
+    are taken from the golden file."""
+    import json
+    import os
+    from paper_2001_10635_b200 import driver as D
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "io")
+    m = pk.make_traffic(5)
+    prob = pk.ReachProblem(m, pk.IntervalVector(np.full(5, 10.0), np.full(5, 20.0)),
+                           pk.IntervalVector([4.0], [6.0]), 0.0, 3.0, 0.5, 2)
+    tube = D.dispatch("mixed-monotonicity", prob, ctx=ctx)
+    with open(os.path.join(gold, "traffic_mm.csv")) as f:
+        assert D.tube_to_csv(tube) == f.read()
+    with open(os.path.join(gold, "traffic_mm.json")) as f:
+        text = f.read()
+    ref_rep = json.loads(text)["report"]
+    for k in ("method", "n", "m", "workers", "steps", "peak_state_bytes"):
+        assert getattr(tube.report, k) == ref_rep[k], k
+    ph = ref_rep["phases"]
+    tube.report.phases = pk.PhaseTimes(ph["setup_s"], ph["integration_s"], ph["reduction_s"])
+    assert D.tube_to_json(tube) == text
+
+
+def test_driver_bench_sweep_on_device(ctx):
+    """driver.bench over two traffic sizes and the CSV the reference's bench
+    command prints."""
+    from paper_2001_10635_b200 import driver as D
+    rows = D.bench("traffic", "mixed-monotonicity", [100, 1000], [1], 2, 0.0, 3.0, 0.5, ctx=ctx)
+    assert [(r.n, r.status, r.steps) for r in rows] == [(100, "ok", 6), (1000, "ok", 6)]
+    lines = D.bench_csv(rows).splitlines()
+    assert lines[0] == "n,workers,median_seconds,steps,status" and len(lines) == 3
