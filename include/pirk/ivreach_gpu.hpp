@@ -25,6 +25,7 @@
 #include <new>
 #include <optional>
 #include <stdexcept>
+#include <cstdio>
 #include <string>
 #include <vector>
 
@@ -279,6 +280,43 @@ inline ReachTube monte_carlo(const ReachProblem& problem, const MonteCarloSpec& 
         return pirk_monte_carlo(c, m, p, &s, tb, r);
     });
     return t;
+}
+
+// driver.cpp:28-34: route a method name to its entry point.
+inline ReachTube dispatch(const std::string& method, const ReachProblem& problem, const MonteCarloSpec& mc,
+                          int workers) {
+    if (method == "growth-bound") return growth_bound(problem, workers);
+    if (method == "mixed-monotonicity") return mixed_monotonicity(problem, workers);
+    if (method == "monte-carlo") return monte_carlo(problem, mc, workers);
+    throw std::invalid_argument("unknown method: " + method);
+}
+
+// io.cpp:84-103: `t,lower0,upper0,...` with %.17g values, byte-identical to
+// the reference's tube_to_csv.
+inline std::string tube_to_csv(const ReachTube& tube) {
+    auto put = [](std::string& out, double v) {
+        char buf[32];
+        std::snprintf(buf, sizeof(buf), "%.17g", v);
+        out += buf;
+    };
+    std::string out = "t";
+    const std::size_t n = tube.entries.empty() ? 0 : tube.entries.front().box.dim();
+    for (std::size_t i = 0; i < n; ++i) {
+        out += ",lower" + std::to_string(i);
+        out += ",upper" + std::to_string(i);
+    }
+    out += "\n";
+    for (const auto& e : tube.entries) {
+        put(out, e.t);
+        for (std::size_t i = 0; i < e.box.dim(); ++i) {
+            out += ',';
+            put(out, e.box.lower(i));
+            out += ',';
+            put(out, e.box.upper(i));
+        }
+        out += '\n';
+    }
+    return out;
 }
 
 }  // namespace ivreach

@@ -3,7 +3,10 @@
 // run on the GPU.  Prints one line per check; exit code = number of failures.
 #include <cmath>
 #include <cstdio>
+#include <fstream>
+#include <sstream>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "pirk/ivreach_gpu.hpp"
@@ -17,8 +20,9 @@ static void check(bool ok, const char* what) {
     if (!ok) ++failures;
 }
 
-int main() {
+int main(int argc, char** argv) {
     const double kE = 2.718281828459045;
+    const std::string golden = argc > 1 ? argv[1] : "";  // tests/golden/io/traffic_mm.csv
     {   // test_reach.cpp:70-75
         ReachProblem p{make_scalar_linear(), IntervalVector({1.0}, {2.0}), std::nullopt, 0.0, 1.0, 0.001, 0};
         const ReachTube tube = mixed_monotonicity(p, 1);
@@ -61,6 +65,18 @@ int main() {
         MonteCarloSpec s; s.seed = 42; s.samples_override = 64;
         const ReachTube a = monte_carlo(p, s, 1), b = monte_carlo(p, s, 8);
         check(a.entries.back().box == b.entries.back().box, "monte carlo deterministic across workers");
+    }
+    {   // driver.cpp dispatch + io.cpp tube_to_csv: byte-identical to the reference's file
+        ReachProblem p{make_traffic(5), IntervalVector(std::vector<double>(5, 10.0), std::vector<double>(5, 20.0)),
+                       IntervalVector({4.0}, {6.0}), 0.0, 3.0, 0.5, 2};
+        const ReachTube t = dispatch("mixed-monotonicity", p, MonteCarloSpec{}, 1);
+        std::ifstream f(golden, std::ios::binary);
+        std::stringstream ss;
+        ss << f.rdbuf();
+        check(!golden.empty() && tube_to_csv(t) == ss.str(), "dispatch + tube_to_csv == reference io.cpp bytes");
+        bool threw = false;
+        try { dispatch("bogus", p, MonteCarloSpec{}, 1); } catch (const std::invalid_argument&) { threw = true; }
+        check(threw, "dispatch: unknown method -> invalid_argument");
     }
     return failures;
 }

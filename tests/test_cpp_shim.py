@@ -26,7 +26,8 @@ def test_shim_compiles_and_links(tmp_path):
 @pytest.mark.gpu
 def test_shim_runs_reference_call_sites(tmp_path):
     exe = build(tmp_path)
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    golden = os.path.join(ROOT, "tests", "golden", "io", "traffic_mm.csv")
+    r = subprocess.run([exe, golden], capture_output=True, text=True, timeout=300)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "FAIL" not in r.stdout
