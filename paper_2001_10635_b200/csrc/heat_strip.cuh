@@ -256,9 +256,9 @@ struct HeatStrip {
         // ---- x(j): wait for its box; prefetch x(j+2) into the slot of x(j-2)
         const double* Xj = xslot(xs);
         const double* Xm = xslot((xs + 3) & 3);  // x(j-1)
-        if (has_x) {
-            mbar_wait(bars + xs, (xph >> xs) & 1);
+        if (has_x) {  // issue first: a late x(j) must not delay the prefetch behind it
             if (threadIdx.x == 0 && (!edge || j + 2 < ze)) tma(j + 2, (xs + 2) & 3);
+            mbar_wait(bars + xs, (xph >> xs) & 1);
         }
 
         // ---- stage 1 at p = j-1: centre and base x(j-1), z- x(j-2), z+ x(j)
