@@ -139,6 +139,13 @@ __device__ __forceinline__ void tma_load_plane(double* dst, const void* tmap, in
         : "memory");
 }
 
+// L2 prefetch of the same box (no shared-memory destination, no completion)
+__device__ __forceinline__ void tma_prefetch_l2(const void* tmap, int x, int y, int z) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];\n" ::"l"(tmap), "r"(x), "r"(y),
+                 "r"(z)
+                 : "memory");
+}
+
 // TMEM as per-thread pipeline storage: each warp owns a 32-lane quadrant
 // (warp % 4) and a 128-column slice (warp / 4) of the CTA's 512 columns; a
 // thread keeps its two RK accumulators per plane in flight there (4 planes x

@@ -58,6 +58,9 @@
 #ifndef PIRK_STRIP_CSE
 #define PIRK_STRIP_CSE 1   // interior tiles share anti-diagonal pair sums
 #endif
+#ifndef PIRK_STRIP_L2PF
+#define PIRK_STRIP_L2PF 0  // L2 prefetch of x planes beyond the smem ring (measured: 1, 2, 4 planes all slightly slower)
+#endif
 #ifndef PIRK_STRIP_S4SKIP
 #define PIRK_STRIP_S4SKIP 0  // halo warps 0 and 15 skip stage 4 (measured slower: 7.40 vs 6.55 ms, g=800)
 #endif
@@ -258,6 +261,8 @@ struct HeatStrip {
         const double* Xm = xslot((xs + 3) & 3);  // x(j-1)
         if (has_x) {  // issue first: a late x(j) must not delay the prefetch behind it
             if (threadIdx.x == 0 && (!edge || j + 2 < ze)) tma(j + 2, (xs + 2) & 3);
+            if (PIRK_STRIP_L2PF > 0 && threadIdx.x == 0 && j + 2 + PIRK_STRIP_L2PF < ze)
+                tma_prefetch_l2(tmap, bx0, by0, j + 2 + PIRK_STRIP_L2PF - wbz);  // warm L2 further ahead
             mbar_wait(bars + xs, (xph >> xs) & 1);
         }
 
