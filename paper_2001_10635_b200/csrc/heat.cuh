@@ -347,12 +347,10 @@ struct HeatRun {
         const int X0 = xbuf(x8), X1 = xbuf((x8 + 7) & 7), X3 = xbuf((x8 + 5) & 7),
                   X4 = xbuf((x8 + 4) & 7);
         if constexpr (Tma) {
-            if (j < ze) mbar_wait(bars + x8, ((j - zs) >> 3) & 1);  // x(j) landed
-        }
-        if constexpr (Tma) {
             // three planes of prefetch: x(j+3) into the slot of x(j-5), last read
-            // (stage 4) in iteration j-1
+            // (stage 4) in iteration j-1; issued before waiting for x(j)
             if (j + 3 < ze) load(nullptr, j + 3, (x8 + 3) & 7);
+            if (j < ze) mbar_wait(bars + x8, ((j - zs) >> 3) & 1);  // x(j) landed
         } else {
             if (j + 1 < ze) load(ldp, j + 1, (x8 + 1) & 7);  // x(j+1) into the slot of x(j-7)
         }
@@ -657,8 +655,9 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
     tmem_fence_before();
     __syncthreads();
     tmem_fence_after();
-    const unsigned tacc = tmem_base + (static_cast<unsigned>(32 * (warp & 3)) << 16) +
-                          static_cast<unsigned>(128 * (warp >> 2));
+    // (through a warp reduction: the base then sits in a uniform register)
+    const unsigned tacc = __reduce_or_sync(0xffffffffu, tmem_base + (static_cast<unsigned>(32 * (warp & 3)) << 16) +
+                                                            static_cast<unsigned>(128 * (warp >> 2)));
     const void* tmap = &tm.f[field];
     const int bx0 = static_cast<int>(ix0) - kHeatH, by0 = static_cast<int>(iy0) - kHeatH;
     const int wbz = static_cast<int>(w.win_begin);

@@ -212,8 +212,8 @@ struct Heat2Run {
         const int x8 = (j - zs) & 7;
         const int X0 = xbuf(x8), X1 = xbuf((x8 + 7) & 7);
         if constexpr (Tma) {
-            if (j < ze) mbar_wait(bars + x8, ((j - zs) >> 3) & 1);
             if (j + 3 < ze) load(nullptr, j + 3, (x8 + 3) & 7);  // into the slot of x(j-5)
+            if (j < ze) mbar_wait(bars + x8, ((j - zs) >> 3) & 1);
         } else {
             if (j + 1 < ze) load(ldp, j + 1, (x8 + 1) & 7);
         }
@@ -538,8 +538,8 @@ heat2_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
     __syncthreads();
     tmem_fence_after();
     // warp w: TMEM lane quadrant w % 4, columns 64 (w / 4) .. +63
-    const unsigned tacc = tmem_base + (static_cast<unsigned>(32 * (warp & 3)) << 16) +
-                          static_cast<unsigned>(64 * (warp >> 2));
+    const unsigned tacc = __reduce_or_sync(0xffffffffu, tmem_base + (static_cast<unsigned>(32 * (warp & 3)) << 16) +
+                                                            static_cast<unsigned>(64 * (warp >> 2)));
     const void* tmap = &tm.f[field];
     const int bx0 = static_cast<int>(ix0) - kHeatH, by0 = static_cast<int>(iy0) - kHeatH;
     const int wbz = static_cast<int>(w.win_begin);
