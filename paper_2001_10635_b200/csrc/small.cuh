@@ -112,6 +112,64 @@ __device__ __forceinline__ void aq_f_all(const SmallModel& m, const double* x, d
     f[11] = kz * x[9] * x[10];
 }
 
+// Fast-mode sin and cos of a small angle (|x| <= 1e5; larger arguments take
+// CUDA's sincos): Cody-Waite reduction by pi/2 in two parts, then the fdlibm /
+// musl kernels __sin and __cos on [-pi/4, pi/4] (error < 1 ulp of the result
+// there).  CUDA's sincos spends most of its instructions on the general
+// Payne-Hanek path (integer ops and branches: profiles/r01_mc_archquad.txt).
+__device__ __forceinline__ void small_sincos(double x, double* s, double* c) {
+    if (!(fabs(x) <= 1e5)) {
+        sincos(x, s, c);
+        return;
+    }
+    const double q = rint(x * 0.63661977236758134308);      // 2/pi
+    double r = fma(-q, 1.57079632673412561417e+00, x);      // pio2_1 (33 bits: exact product)
+    r = fma(-q, 6.07710050650619224932e-11, r);             // pio2_1t
+    const double z = r * r, w = z * z;
+    const double ps = 8.33333333332248946124e-03 + z * (-1.98412698298579493134e-04 + z * 2.75573137070700676789e-06) +
+                      z * w * (-2.50507602534068634195e-08 + z * 1.58969099521155010221e-10);
+    const double sr = r + (z * r) * (-1.66666666666666324348e-01 + z * ps);
+    const double pc = z * (4.16666666666666019037e-02 + z * (-1.38888888888741095749e-03 + z * 2.48015872894767294178e-05)) +
+                      w * w * (-2.75573143513906633035e-07 + z * (2.08757232129817482790e-09 + z * -1.13596475577881948265e-11));
+    const double hz = 0.5 * z, v = 1.0 - hz;
+    const double cr = v + (((1.0 - v) - hz) + z * pc);
+    switch (static_cast<int>(q) & 3) {
+        case 0: *s = sr; *c = cr; break;
+        case 1: *s = cr; *c = -sr; break;
+        case 2: *s = -sr; *c = -cr; break;
+        default: *s = -cr; *c = sr; break;
+    }
+}
+
+// arch-quadrotor in fast mode: the same field with small_sincos, one 1/cos
+// and the constant quotients folded (tolerance-only in both modes: glibc and
+// CUDA trig differ in the last ulp, DESIGN.md (c))
+__device__ __forceinline__ void aq_f_all_fast(const SmallModel& m, const double* x, double* f) {
+    const double mass = m.P[0], gravity = m.P[1], jx = m.P[2], jy = m.P[3], jz = m.P[4];
+    const double kx = (jy - jz) / jx, ky = (jz - jx) / jy, kz = (jx - jy) / jz;  // uniform: hoisted
+    const double ijx = 1.0 / jx, ijy = 1.0 / jy, imass = 1.0 / mass;
+    double s7, c7, s8, c8, s9, c9;
+    small_sincos(x[6], &s7, &c7);
+    small_sincos(x[7], &s8, &c8);
+    small_sincos(x[8], &s9, &c9);
+    const double ic8 = 1.0 / c8, t8 = s8 * ic8;
+    f[0] = c8 * c9 * x[3] + (s7 * s8 * c9 - c7 * s9) * x[4] + (c7 * s8 * c9 + s7 * s9) * x[5];
+    f[1] = c8 * s9 * x[3] + (s7 * s8 * s9 + c7 * c9) * x[4] + (c7 * s8 * s9 - s7 * c9) * x[5];
+    f[2] = s8 * x[3] - s7 * c8 * x[4] - c7 * c8 * x[5];
+    f[3] = x[11] * x[4] - x[10] * x[5] - gravity * s8;
+    f[4] = x[9] * x[5] - x[11] * x[3] + gravity * c8 * s7;
+    {
+        const double thrust = mass * gravity - 10.0 * (x[2] - 1.0) + 3.0 * x[5];
+        f[5] = x[10] * x[3] - x[9] * x[4] + gravity * c8 * c7 - thrust * imass;
+    }
+    f[6] = x[9] + s7 * t8 * x[10] + c7 * t8 * x[11];
+    f[7] = c7 * x[10] - s7 * x[11];
+    f[8] = s7 * ic8 * x[10] + c7 * ic8 * x[11];
+    f[9] = kx * x[10] * x[11] - (x[6] + x[9]) * ijx;
+    f[10] = ky * x[9] * x[11] - (x[7] + x[10]) * ijy;
+    f[11] = kz * x[9] * x[10];
+}
+
 __device__ __forceinline__ void ll_f_all(const double* x, double* f) {
     f[0] = 1.4 * x[2] - 0.9 * x[0];
     f[1] = 2.5 * x[4] - 1.5 * x[1];
@@ -256,10 +314,11 @@ cudaError_t launch_small_integrate(const SmallModel& m, int which, const double*
 constexpr int kMcThreads = 128;
 
 // Functors giving f for a compile-time dimension (N > 0) or the generic path.
-template <int N>
+template <int N, bool Exact>
 struct McField {
     __device__ static void eval(const SmallModel& m, const double* x, const double* p, double* f) {
-        if constexpr (N == 12) aq_f_all(m, x, f);
+        if constexpr (N == 12 && !Exact) aq_f_all_fast(m, x, f);
+        else if constexpr (N == 12) aq_f_all(m, x, f);
         else if constexpr (N == 7) ll_f_all(x, f);
         else sm_f_all(m, x, p, f);
     }
@@ -335,19 +394,19 @@ monte_carlo_kernel(const SmallModel m, const McArgs a) {
     for (unsigned long long st = 0; st < a.total; ++st) {
         const StepConsts c = step_consts(a.t0, a.t1, a.h, st, a.total);
         if (active && !dead) {
-            McField<N>::eval(m, x, p, k);
+            McField<N, Exact>::eval(m, x, p, k);
 #pragma unroll
             for (int i = 0; i < NA; ++i)
                 if (i < n) { acc[i] = k[i]; u[i] = x[i] + c.h2 * k[i]; }
-            McField<N>::eval(m, u, p, k);
+            McField<N, Exact>::eval(m, u, p, k);
 #pragma unroll
             for (int i = 0; i < NA; ++i)
                 if (i < n) { acc[i] = acc[i] + 2.0 * k[i]; u[i] = x[i] + c.h2 * k[i]; }
-            McField<N>::eval(m, u, p, k);
+            McField<N, Exact>::eval(m, u, p, k);
 #pragma unroll
             for (int i = 0; i < NA; ++i)
                 if (i < n) { acc[i] = acc[i] + 2.0 * k[i]; u[i] = x[i] + c.hk * k[i]; }
-            McField<N>::eval(m, u, p, k);
+            McField<N, Exact>::eval(m, u, p, k);
 #pragma unroll
             for (int i = 0; i < NA; ++i)
                 if (i < n) x[i] = x[i] + c.h6 * (acc[i] + k[i]);

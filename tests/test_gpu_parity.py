@@ -285,6 +285,14 @@ def test_arch_quad_mc_tolerance(ctx):
     assert_within(tube, mc_oracle(prob, 1, 4096), rel=1e-12, atol=1e-14, never_tighter=False)
 
 
+def test_arch_quad_mc_fast_mode_tolerance(fast_ctx):
+    """Fast mode: small-angle sincos and folded quotients in the arch-quadrotor
+    field (csrc/small.cuh aq_f_all_fast), against the glibc-trig oracle."""
+    m, prob = arch_quad_problem()
+    tube = pk.monte_carlo(prob, pk.MonteCarloSpec(seed=1, samples_override=4096), ctx=fast_ctx)
+    assert_within(tube, mc_oracle(prob, 1, 4096), rel=1e-12, atol=1e-14, never_tighter=False)
+
+
 def test_mc_hull_inside_exact_image(ctx):
     # test_reach.cpp:113-124
     m = pk.make_scalar_linear()
