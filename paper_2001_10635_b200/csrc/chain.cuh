@@ -16,6 +16,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -294,7 +295,10 @@ chain_warp_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc,
         last |= static_cast<unsigned>(g0 + k + 1 == n) << k;
     }
     const unsigned full = 0xffffffffu;
-
+    // The boundary flags matter only in the (at most two) warps holding
+    // component 0 or n-1: every other warp runs the stages without them.
+    auto stages = [&](auto edge_tag) {
+    constexpr bool Edge = decltype(edge_tag)::value;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
         double k0[kCwP], k1[kCwP];
@@ -319,7 +323,7 @@ chain_warp_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc,
             }
 #pragma unroll
             for (int k = 0; k < kCwP; ++k) {
-                const bool fs = (first >> k) & 1, ls = (last >> k) & 1;
+                const bool fs = Edge && ((first >> k) & 1), ls = Edge && ((last >> k) & 1);
                 {  // models.cpp:68-74, one flux per edge shared by its two ends
                     const double in = fs ? beta * m.p0 : beta * (k ? F0[k - 1] : l0);
                     const double out = ls ? ref_min(c, v * u0[k]) : F0[k];
@@ -347,7 +351,7 @@ chain_warp_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc,
             const double S0r = __shfl_down_sync(full, S0[0], 1), S1r = __shfl_down_sync(full, S1[0], 1);
 #pragma unroll
             for (int k = 0; k < kCwP; ++k) {
-                const bool fs = (first >> k) & 1, ls = (last >> k) & 1;
+                const bool fs = Edge && ((first >> k) & 1), ls = Edge && ((last >> k) & 1);
                 {
                     const double sl = fs ? 0.0 : (k ? S0[k - 1] : S0l);
                     const double sr = ls ? 0.0 : (k + 1 < kCwP ? S1[k + 1] : S1r);
@@ -383,6 +387,11 @@ chain_warp_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc,
             }
         }
     }
+    };
+    if (__any_sync(full, (first | last) != 0))
+        stages(std::true_type{});
+    else
+        stages(std::false_type{});
 
     // ---- store the segment's outputs (lanes 1..30) and flag non-finite values
     if (lane == 0 || lane == 31) return;
