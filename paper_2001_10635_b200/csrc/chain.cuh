@@ -422,15 +422,13 @@ cudaError_t launch_chain_step(const ChainModel& m, const WindowArgs& w, const St
                               cudaStream_t stream) {
     if (w.out_end <= w.out_begin) return cudaSuccess;
     const uint64_t count = w.out_end - w.out_begin;
-    // Fast mode: the warp-tiled kernel (n = 1e7: traffic 0.110 vs 0.139 ms,
-    // chain 0.114 vs 0.135 ms).  Exact mode: the shared-memory tile kernel
-    // (its IEEE divisions run faster there: chain 0.163 vs 0.199 ms).
-    // PIRK_CHAIN_KERNEL=smem|warp overrides (A/B comparisons, parity tests).
+    // The warp-tiled kernel in both modes (n = 1e7, ms per step, warp vs smem
+    // tiles: fast traffic 0.097 vs 0.139, chain 0.0995 vs 0.135; exact traffic
+    // 0.165 vs 0.202, chain 0.153 vs 0.163).  PIRK_CHAIN_KERNEL=smem|warp
+    // overrides (A/B comparisons, parity tests of both kernels).
     static const bool use_smem = [] {
         const char* v = std::getenv("PIRK_CHAIN_KERNEL");
-        if (v && std::strcmp(v, "smem") == 0) return true;
-        if (v && std::strcmp(v, "warp") == 0) return false;
-        return Exact;
+        return v && std::strcmp(v, "smem") == 0;
     }();
     if (!use_smem) {
         const uint64_t per_block = static_cast<uint64_t>(kCwWarps) * kCwOut;
