@@ -240,10 +240,17 @@ def cpu_baseline(args):
     r = O.ref_reach(O.METHOD_MM, model, np.full(n, 0.9), np.full(n, 1.1), None, None, 0.0,
                     steps * args.h, args.h, 0, workers=threads, keep=False)
     rate = 2.0 * n * steps / r.report["integration_s"]
+    # the same reference on one worker (all cores and 1), over a
+    # quarter of the sample's steps to stay within the bench's time budget
+    s1 = max(1, steps // 4)
+    r1 = O.ref_reach(O.METHOD_MM, model, np.full(n, 0.9), np.full(n, 1.1), None, None, 0.0,
+                     s1 * args.h, args.h, 0, workers=1, keep=False)
     return {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
             "sample": f"ivreach::mixed_monotonicity (oracle/_ref, -O3, OpenMP) heat3d grid={g} "
                       f"(n={n}), {steps} RK4 steps, h={args.h}; rate = 2n*steps/integration_s",
-            "wall_s": r.wall_s}
+            "wall_s": r.wall_s,
+            "single_worker": {"value": 2.0 * n * s1 / r1.report["integration_s"], "cores": 1,
+                              "steps": s1}}
 
 
 def secondary(args, pk, torch):
