@@ -452,3 +452,93 @@ def test_driver_bench_sweep_on_device(ctx):
     assert [(r.n, r.status, r.steps) for r in rows] == [(100, "ok", 6), (1000, "ok", 6)]
     lines = D.bench_csv(rows).splitlines()
     assert lines[0] == "n,workers,median_seconds,steps,status" and len(lines) == 3
+
+
+# ------------------------------------------------------------ sharded windows
+
+class _NoopExchanger:
+    """Halo exchange stand-in for virtual ranks on one device: the test copies
+    the halos before each exchange step, so start/finish only mark the split
+    (interior launch, then boundary launches) that ShardedReach.run makes."""
+
+    def start(self, fields):
+        return None
+
+    def finish(self, handle):
+        pass
+
+    def exchange(self, fields):
+        pass
+
+
+def _fill_halos(runs, unit):
+    """Copy every rank's owned boundary units into its neighbours' halos."""
+    for r, run in enumerate(runs):
+        s = run.shard
+        for nb in (r - 1, r + 1):
+            if nb < 0 or nb >= len(runs):
+                continue
+            o = runs[nb].shard
+            lo, hi = (s.win_begin, s.begin) if nb == r - 1 else (s.end, s.win_end)
+            for f in (0, 1):
+                src = runs[nb].a[f][(lo - o.win_begin) * unit:(hi - o.win_begin) * unit]
+                run.a[f][(lo - s.win_begin) * unit:(hi - s.win_begin) * unit].copy_(src)
+
+
+@pytest.mark.parametrize("kind,world,K,mode", [("heat", 3, 1, "fast"), ("heat", 3, 2, "exact"),
+                                               ("heat", 2, 1, "exact"), ("traffic", 3, 2, "fast"),
+                                               ("chain", 2, 1, "exact")])
+def test_sharded_windows_on_device(kind, world, K, mode):
+    """The N>1 data path on one B200: virtual ranks run ShardedReach with the
+    CUDA windowed step (interior launch + boundary launches on exchange steps,
+    deep halos for K > 1) and reproduce the single-device reach bit for bit --
+    the windowed heat strip / chain warp kernels compute each unit exactly as
+    the full-domain launch does."""
+    import torch
+    from paper_2001_10635_b200 import sharded as S
+    c = pk.Context(0, mode)
+    try:
+        if kind == "heat":
+            g = 64
+            m = pk.make_heat3d(g)
+            n = m.dim
+            lo = 0.9 - 0.05 * ((np.arange(n) * 7) % 5)
+            hi = lo + 0.2
+            plo = phi = None
+            h = 0.2 / (g - 1) ** 2
+            t1 = 6 * h
+        else:
+            n = 5000
+            m = pk.make_traffic(n) if kind == "traffic" else pk.make_chain(n)
+            lo = (10.0 if kind == "traffic" else -0.05) + 0.001 * (np.arange(n) % 7)
+            hi = lo + (10.0 if kind == "traffic" else 0.1)
+            plo, phi = ([4.0], [6.0]) if kind == "traffic" else ([-0.1], [0.1])
+            h, t1 = (0.5, 3.0) if kind == "traffic" else (0.01, 0.06)
+        prob = pk.ReachProblem(m, pk.IntervalVector(lo, hi), pk.IntervalVector(plo, phi) if plo else None,
+                               0.0, t1, h, 0)
+        ref = pk.mixed_monotonicity(prob, ctx=c).entries[-1].box
+        units, unit = S.units_of(m)
+        step = S.device_step_fn(m, "mixed-monotonicity", c)
+        runs = []
+        for r in range(world):
+            sh = S.Shard(units, world, r, 4 * K)
+            run = S.ShardedReach(m, "mixed-monotonicity", sh, step, _NoopExchanger(), plo, phi, K=K)
+            run.alloc(lambda k: torch.full((k,), float("nan"), dtype=torch.float64, device="cuda"))
+            sl = slice(sh.win_begin * unit, sh.win_end * unit)
+            run.a[0].copy_(torch.from_numpy(np.ascontiguousarray(lo[sl])))
+            run.a[1].copy_(torch.from_numpy(np.ascontiguousarray(hi[sl])))
+            runs.append(run)
+        for i, (t, hk) in enumerate(S.plan_rk4_steps(0.0, t1, h)):
+            if i % K == 0:
+                _fill_halos(runs, unit)
+            for run in runs:
+                run.run([(t, hk)], i)
+        torch.cuda.synchronize()
+        got_lo, got_hi = np.empty(n), np.empty(n)
+        for run in runs:
+            o0, o1 = run.owned()
+            b, e = run.shard.begin * unit, run.shard.end * unit
+            got_lo[b:e], got_hi[b:e] = o0.cpu().numpy(), o1.cpu().numpy()
+        assert np.array_equal(got_lo, ref.lower) and np.array_equal(got_hi, ref.upper)
+    finally:
+        c.close()
