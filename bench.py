@@ -209,6 +209,10 @@ def heat_e2e(args, pk, torch, world):
                            C5_STEPS * args.h, args.h, 0)
     ctx = pk.get_context(0)
     ctx.set_mode(args.mode)
+    # one untimed call first: the driver maps freshly registered host pages on
+    # their first DMA (the first upload of each 32 GB buffer runs synchronously),
+    # which is setup like the registration itself, not per-call work
+    pk.mixed_monotonicity(prob, ctx=ctx, out=(olo, ohi))
     t0 = time.perf_counter()
     tube = pk.mixed_monotonicity(prob, ctx=ctx, out=(olo, ohi))
     dt = time.perf_counter() - t0
@@ -216,7 +220,9 @@ def heat_e2e(args, pk, torch, world):
     res = {"value": 2.0 * n * steps / dt, "unit": UNIT, "h2d_bytes_per_step": 2 * n * 8,
            "d2h_bytes_per_step": 2 * n * 8, "seconds": dt, "rk4_steps": steps,
            "n": n, "grid": g, "api": "paper_2001_10635_b200.mixed_monotonicity",
-           "step": "one full C5 reach call (H2D initial box, 100 RK4 steps, order check, D2H final box)"}
+           "step": "one full C5 reach call (H2D initial box, 100 RK4 steps, order check, D2H final box); "
+                   "lower field integrated while the upper field uploads, downloaded while it integrates",
+           "warmup_calls": 1}
     ok = bool(np.isfinite(olo[:: max(1, n // 4096)]).all())
     del tube, prob, lo, hi, olo, ohi
     for b in bufs:

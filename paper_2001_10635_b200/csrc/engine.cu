@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -461,9 +462,160 @@ pirk_status engine_advance(pirk_engine* e, uint64_t nsteps) {
     return PIRK_OK;
 }
 
+// RAII for the pipelined path's extra stream and events
+struct StreamGuard {
+    cudaStream_t s = nullptr;
+    ~StreamGuard() { if (s) cudaStreamDestroy(s); }
+};
+struct EventGuard {
+    cudaEvent_t e = nullptr;
+    ~EventGuard() { if (e) cudaEventDestroy(e); }
+};
+
+// The launcher's kernel choice can be overridden (PIRK_HEAT_BLOCK); one-field
+// launches need the strip kernel.
+bool heat_single_field_ok() {
+    const char* v = std::getenv("PIRK_HEAT_BLOCK");
+    return !v || std::strcmp(v, "strip") == 0;
+}
+
+// heat3d CTMM recording only the final box (tube_stride 0).  The embedding's
+// halves are independent (cooperative decomposition, models.cpp:20-27, and the
+// heat field reads no input), so the lower field is uploaded, integrated and
+// downloaded while the upper field's transfers overlap it on a copy stream:
+//   copy:    H2D lo | H2D hi, box check |            | D2H lo
+//   compute:        | steps lo          | steps hi   | order check, D2H hi
+// Same kernels, same per-unit arithmetic and failure keys (the field-1 keys
+// carry +n as in the two-field launch), so results and error reports are those
+// of run_large; only PCIe time hides behind the integration.
+pirk_status run_heat_mm_pipelined(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p,
+                                  pirk_tube* tube, pirk_report* rep) {
+    const auto t_setup = Clock::now();
+    static const bool trace = std::getenv("PIRK_TRACE") != nullptr;
+    auto mark = [&](const char* what) {
+        if (trace) std::fprintf(stderr, "[pirk] %-24s %8.3f s\n", what, since(t_setup));
+    };
+    const uint64_t launches0 = ctx->launches;
+    pirk_engine e;
+    e.ctx = ctx;
+    e.model = *m;
+    e.method = PIRK_METHOD_MM;
+    e.t0 = p->t0;
+    e.t1 = p->t1;
+    e.h = p->h;
+    plan_steps(p->t0, p->t1, p->h, e.plan);
+    if (e.plan.total >= (1ull << 23))
+        return fail(ctx, PIRK_EINVAL, "step count exceeds the device failure-key range (2^23)");
+    e.n = m->dim;
+    e.unit = m->grid * m->grid;
+    e.units = e.n / e.unit;
+    if (2 * e.n >= (1ull << kFailCompBits))
+        return fail(ctx, PIRK_EINVAL, "dimension exceeds the device failure-key range");
+    e.hm = heat_model(m, PIRK_METHOD_MM);
+    const size_t n = e.n;
+    CK(ctx, e.a0.alloc(n));
+    CK(ctx, e.a1.alloc(n));
+    CK(ctx, e.b0.alloc(n));
+    CK(ctx, e.b1.alloc(n));
+    CK(ctx, e.d_fail.alloc(2));
+    DevBuf<unsigned long long> flag;  // [0] box check, [1] order check
+    CK(ctx, flag.alloc(2));
+    StreamGuard xs;
+    CK(ctx, cudaStreamCreateWithFlags(&xs.s, cudaStreamNonBlocking));
+    EventGuard ev_h0, ev_h1, ev_c0, ev_x;
+    for (EventGuard* g : {&ev_h0, &ev_h1, &ev_c0, &ev_x})
+        CK(ctx, cudaEventCreateWithFlags(&g->e, cudaEventDisableTiming));
+    cudaStream_t cs = ctx->stream;
+    CK(ctx, cudaMemsetAsync(e.d_fail.p, 0xff, 2 * sizeof(unsigned long long), cs));
+    CK(ctx, cudaMemsetAsync(flag.p, 0xff, 2 * sizeof(unsigned long long), cs));
+    mark("allocated");
+    CK(ctx, cudaEventRecord(ev_x.e, cs));
+    CK(ctx, cudaStreamWaitEvent(xs.s, ev_x.e, 0));
+    CK(ctx, cudaMemcpyAsync(e.a0.p, p->init_lower, n * sizeof(double), cudaMemcpyHostToDevice, xs.s));
+    CK(ctx, cudaEventRecord(ev_h0.e, xs.s));
+    CK(ctx, cudaMemcpyAsync(e.a1.p, p->init_upper, n * sizeof(double), cudaMemcpyHostToDevice, xs.s));
+    CK(ctx, launch_box_check(e.a0.p, e.a1.p, n, flag.p, xs.s));  // interval.cpp:14-22
+    ctx->launches++;
+    CK(ctx, cudaEventRecord(ev_h1.e, xs.s));
+    mark("uploads enqueued");
+    const double setup_s = since(t_setup);
+
+    const auto t_int = Clock::now();
+    double* fin[2] = {nullptr, nullptr};
+    for (int f = 0; f < 2; ++f) {
+        CK(ctx, cudaStreamWaitEvent(cs, f == 0 ? ev_h0.e : ev_h1.e, 0));
+        double* a = f == 0 ? e.a0.p : e.a1.p;
+        double* b = f == 0 ? e.b0.p : e.b1.p;
+        for (uint64_t k = 0; k < e.plan.total; ++k) {
+            const StepConsts sc = host_step(e.t0, e.t1, e.h, k, e.plan.total);
+            WindowArgs w = f == 0 ? WindowArgs{a, a, b, b, 0, e.units, 0, e.units}
+                                  : WindowArgs{a, a, b, b, 0, e.units, 0, e.units};
+            ctx->launches++;
+            CK(ctx, exact_mode(ctx) ? launch_heat_step<true>(e.hm, w, sc, k, e.d_fail.p, cs, f)
+                                    : launch_heat_step<false>(e.hm, w, sc, k, e.d_fail.p, cs, f));
+            std::swap(a, b);
+        }
+        fin[f] = a;
+        if (f == 0) {  // the lower field's box leaves while the upper one integrates
+            CK(ctx, cudaEventRecord(ev_c0.e, cs));
+            CK(ctx, cudaStreamWaitEvent(xs.s, ev_c0.e, 0));
+            CK(ctx, cudaMemcpyAsync(tube->lower, fin[0], n * sizeof(double), cudaMemcpyDeviceToHost, xs.s));
+        }
+    }
+    CK(ctx, launch_order_check(fin[0], fin[1], n, flag.p + 1, cs));  // reach.cpp:181-186
+    ctx->launches++;
+    CK(ctx, cudaMemcpyAsync(tube->upper, fin[1], n * sizeof(double), cudaMemcpyDeviceToHost, cs));
+    unsigned long long hf[4];
+    CK(ctx, cudaMemcpyAsync(hf, e.d_fail.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs));
+    CK(ctx, cudaMemcpyAsync(hf + 2, flag.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs));
+    mark("all enqueued");
+    CK(ctx, cudaStreamSynchronize(cs));
+    mark("compute stream done");
+    CK(ctx, cudaStreamSynchronize(xs.s));
+    mark("copy stream done");
+    const double integ_s = since(t_int);
+
+    if (hf[2] != kNoFail) {  // the box is validated before anything else (interval.cpp:14-22)
+        const uint64_t i = hf[2];
+        const bool nonfinite = !std::isfinite(p->init_lower[i]) || !std::isfinite(p->init_upper[i]);
+        return fail(ctx, PIRK_EINVAL, std::string(nonfinite ? "interval: non-finite bound at component "
+                                                            : "interval: lower > upper at component ") +
+                                          std::to_string(i));
+    }
+    tube->n_slots = 1;
+    if (tube->times) tube->times[0] = p->t1;
+    if (hf[0] != kNoFail) {
+        const uint64_t fs = hf[0] >> kFailCompBits, fc = hf[0] & ((1ull << kFailCompBits) - 1);
+        return fail(ctx, PIRK_EINTEGRATION, "mixed-monotonicity embedding integration: " +
+                                                integ_msg(fs, fc, p->t0 + static_cast<double>(fs) * p->h));
+    }
+    if (hf[3] != kNoFail)
+        return fail(ctx, PIRK_EORDER, "mixed-monotonicity: embedding order violated at step " +
+                                          std::to_string(e.plan.total) + ", t = " + fstr(p->t1) +
+                                          ", component " + std::to_string(hf[3]));
+    fill_report(rep, n, 0, e.plan.total, 7 * 2 * n * sizeof(double), 4 * n * sizeof(double), exact_mode(ctx),
+                setup_s, integ_s, 0.0, ctx->launches - launches0);
+    return PIRK_OK;
+}
+
 // Large-model (chain / heat kernels) MM and GB driver.
 pirk_status run_large(pirk_ctx* ctx, const pirk_model* m, int method, const pirk_problem* p,
                       pirk_tube* tube, pirk_report* rep) {
+    {   // heat3d CTMM with only the final box: field-pipelined transfers
+        Plan pl;
+        plan_steps(p->t0, p->t1, p->h, pl);
+        std::vector<uint64_t> ss;
+        std::vector<double> st;
+        record_schedule(p->t0, p->t1, p->h, p->tube_stride, pl, ss, st);
+        static const bool pipelined = [] {
+            const char* v = std::getenv("PIRK_PIPELINE");
+            return !(v && std::strcmp(v, "0") == 0);
+        }();
+        if (pipelined && is_heat(m) && method == PIRK_METHOD_MM && ss.size() == 1 && tube && tube->lower &&
+            tube->upper && tube->max_slots >= 1 && m->dim >= (1ull << 22) && !exact_mode(ctx) &&
+            m->grid % 2 == 0 && heat_single_field_ok())
+            return run_heat_mm_pipelined(ctx, m, p, tube, rep);
+    }
     const auto t_setup = Clock::now();
     const uint64_t launches0 = ctx->launches;
     pirk_engine e;

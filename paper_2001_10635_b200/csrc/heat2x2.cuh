@@ -568,8 +568,8 @@ heat2_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
 
 // z-chunk length for one-CTA-per-SM heat kernels over tx x tx tiles and two
 // fields: the count minimising waves x (planes per chunk + 8 halo planes
-// recomputed per chunk), i.e. the wave quantisation of 2 tx^2 CTAs per chunk
-inline uint64_t heat_zchunk(uint64_t tx, uint64_t planes, int n_sm) {
+// recomputed per chunk), i.e. the wave quantisation of nf tx^2 CTAs per chunk
+inline uint64_t heat_zchunk(uint64_t tx, uint64_t planes, int n_sm, unsigned nf = 2) {
     static const int forced = [] {  // PIRK_HEAT_ZCHUNKS=c forces c chunks (A/B only)
         const char* v = std::getenv("PIRK_HEAT_ZCHUNKS");
         return v ? std::atoi(v) : 0;
@@ -579,7 +579,7 @@ inline uint64_t heat_zchunk(uint64_t tx, uint64_t planes, int n_sm) {
     double best_cost = 0.0;
     for (uint64_t c = 1; c <= 8 && c <= planes; ++c) {
         const uint64_t zc = (planes + c - 1) / c;
-        const uint64_t ctas = tx * tx * 2 * ((planes + zc - 1) / zc);
+        const uint64_t ctas = tx * tx * nf * ((planes + zc - 1) / zc);
         const double cost = static_cast<double>((ctas + n_sm - 1) / n_sm) *
                             static_cast<double>(zc + (c > 1 ? 2 * kHeatH : 0));
         if (c == 1 || cost < best_cost) best = c, best_cost = cost;
@@ -590,8 +590,11 @@ inline uint64_t heat_zchunk(uint64_t tx, uint64_t planes, int n_sm) {
 template <bool Exact>
 cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const StepConsts& sc,
                              unsigned long long step, unsigned long long* fail,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, int field_only) {
     if (w.out_end <= w.out_begin) return cudaSuccess;
+    // field_only >= 0: advance that field alone (grid z = chunks, flags bit 2 + index)
+    const unsigned nf = field_only < 0 ? 2u : 1u;
+    const int fsel = field_only < 0 ? 0 : (4 | ((field_only & 1) << 3));
     // Kernel variant.  Fast mode: warp-wide strips with TMEM histories
     // (heat_strip.cuh) whenever its TMA path is available (even g, aligned
     // windows), else 2x2 blocks.  Exact mode: 1x2 pairs (its longer per-point
@@ -606,6 +609,10 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
         if (v && std::strcmp(v, "strip") == 0) return 3;
         return Exact ? 0 : 3;
     }();
+    // one-field launches exist for the strip kernel only (fast mode, even g);
+    // the engine's field-pipelined driver checks that before using them
+    if (field_only >= 0 && (Exact || variant != 3 || m.g % 2 != 0)) return cudaErrorInvalidValue;
+
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(heat_step_kernel<Exact>,
@@ -619,8 +626,11 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
                 e = cudaFuncSetAttribute(heat4_step_kernel<Exact>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(k4SmemBytes));
             if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(heat_strip_kernel<Exact>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSSmemBytes));
+                e = cudaFuncSetAttribute(heat_strip_kernel<Exact, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSSmemBytes));
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(heat_strip_kernel<Exact, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSSmemBytes));
         }
         if (e != cudaSuccess) return e;
         attr_set = true;
@@ -651,11 +661,15 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
         if (variant == 3 && heat_encode_tmap(&tm.f[0], w.in0, m.g, wplanes, kSF, kSF) &&
             heat_encode_tmap(&tm.f[1], w.in1, m.g, wplanes, kSF, kSF)) {
             const uint64_t tx = (m.g + kST - 1) / kST;
-            const uint64_t zchunk = heat_zchunk(tx, planes, n_sm);
+            const uint64_t zchunk = heat_zchunk(tx, planes, n_sm, nf);
             const uint64_t nchunks = (planes + zchunk - 1) / zchunk;
-            dim3 grid(static_cast<unsigned>(tx), static_cast<unsigned>(tx), static_cast<unsigned>(2 * nchunks));
-            heat_strip_kernel<Exact><<<grid, kSThreads, kSSmemBytes, stream>>>(m, hp, w, sc, step, zchunk, fail,
-                                                                                tm, 1 | (vec ? 2 : 0));
+            dim3 grid(static_cast<unsigned>(tx), static_cast<unsigned>(tx), static_cast<unsigned>(nf * nchunks));
+            if (field_only >= 0)
+                heat_strip_kernel<Exact, true><<<grid, kSThreads, kSSmemBytes, stream>>>(
+                    m, hp, w, sc, step, zchunk, fail, tm, 1 | (vec ? 2 : 0) | fsel);
+            else
+                heat_strip_kernel<Exact, false><<<grid, kSThreads, kSSmemBytes, stream>>>(
+                    m, hp, w, sc, step, zchunk, fail, tm, 1 | (vec ? 2 : 0));
             return cudaGetLastError();
         }
         std::memset(&tm, 0, sizeof tm);
@@ -663,9 +677,9 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
         if (variant == 2 && m.g % 2 == 0 && reinterpret_cast<uintptr_t>(w.in0) % 16 == 0 &&
             reinterpret_cast<uintptr_t>(w.in1) % 16 == 0) {
             const uint64_t tx = (m.g + k4T - 1) / k4T;
-            const uint64_t zchunk = heat_zchunk(tx, planes, n_sm);
+            const uint64_t zchunk = heat_zchunk(tx, planes, n_sm, nf);
             const uint64_t nchunks = (planes + zchunk - 1) / zchunk;
-            dim3 grid(static_cast<unsigned>(tx), static_cast<unsigned>(tx), static_cast<unsigned>(2 * nchunks));
+            dim3 grid(static_cast<unsigned>(tx), static_cast<unsigned>(tx), static_cast<unsigned>(nf * nchunks));
             heat4_step_kernel<Exact><<<grid, k4Threads, k4SmemBytes, stream>>>(m, hp, w, sc, step, zchunk, fail,
                                                                                 tm, 1 | (vec ? 2 : 0));
             return cudaGetLastError();
@@ -675,10 +689,10 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
     // 8-plane halo overhead per chunk small.
     const uint64_t tx = (m.g + kHeatT - 1) / kHeatT;
     uint64_t nchunks = 1;
-    while (tx * tx * 2 * nchunks < 4 * static_cast<uint64_t>(n_sm) && planes / (nchunks * 2) >= 64) nchunks *= 2;
+    while (tx * tx * nf * nchunks < 4 * static_cast<uint64_t>(n_sm) && planes / (nchunks * 2) >= 64) nchunks *= 2;
     const uint64_t zchunk = (planes + nchunks - 1) / nchunks;
     nchunks = (planes + zchunk - 1) / zchunk;
-    dim3 grid(static_cast<unsigned>(tx), static_cast<unsigned>(tx), static_cast<unsigned>(2 * nchunks));
+    dim3 grid(static_cast<unsigned>(tx), static_cast<unsigned>(tx), static_cast<unsigned>(nf * nchunks));
     const int tma = heat_encode_tmap(&tm.f[0], w.in0, m.g, wplanes) &&
                     heat_encode_tmap(&tm.f[1], w.in1, m.g, wplanes);
     if (variant >= 1) {

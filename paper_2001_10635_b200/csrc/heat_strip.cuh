@@ -420,7 +420,7 @@ struct HeatStrip {
     }
 };
 
-template <bool Exact>
+template <bool Exact, bool One = false>
 __global__ void __launch_bounds__(kSThreads, 1)
 heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w, const StepConsts sc,
                   const unsigned long long step, const uint64_t zchunk,
@@ -433,8 +433,11 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
     __shared__ unsigned tmem_base;
     const int tid = threadIdx.x;
     const long long g = static_cast<long long>(m.g);
-    const int field = blockIdx.z & 1;
-    const long long chunk = blockIdx.z >> 1;
+    // One: a single field (index in flags bit 3) per launch, grid z = chunks
+    // (field-pipelined runs); a separate instantiation, so the two-field
+    // kernel is untouched
+    const int field = One ? ((flags >> 3) & 1) : static_cast<int>(blockIdx.z & 1);
+    const long long chunk = One ? static_cast<long long>(blockIdx.z) : static_cast<long long>(blockIdx.z >> 1);
     const long long ix0 = static_cast<long long>(blockIdx.x) * kST;
     const long long iy0 = static_cast<long long>(blockIdx.y) * kST;
     const long long obz = static_cast<long long>(w.out_begin) + chunk * static_cast<long long>(zchunk);

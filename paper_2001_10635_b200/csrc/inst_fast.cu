@@ -11,7 +11,7 @@ template cudaError_t launch_chain_step<false>(const ChainModel&, const WindowArg
                                               unsigned long long*, cudaStream_t);
 template cudaError_t launch_heat_step<false>(const HeatModel&, const WindowArgs&,
                                              const StepConsts&, unsigned long long,
-                                             unsigned long long*, cudaStream_t);
+                                             unsigned long long*, cudaStream_t, int);
 template cudaError_t launch_small_integrate<false>(const SmallModel&, int, const double*,
                                                    const double*, double, double, double,
                                                    unsigned long long, unsigned long long,

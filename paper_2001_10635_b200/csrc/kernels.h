@@ -58,7 +58,7 @@ cudaError_t launch_chain_step(const ChainModel& m, const WindowArgs& w, const St
 template <bool Exact>
 cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const StepConsts& sc,
                              unsigned long long step, unsigned long long* fail,
-                             cudaStream_t stream);
+                             cudaStream_t stream, int field_only = -1);
 
 // which: 0 = f under p, 1 = growth under w, 2 = embedding (dim 2n, p = [p_lo | p_hi]).
 // One thread integrates the whole plan, recording `slots` states into rec.

@@ -542,3 +542,35 @@ def test_sharded_windows_on_device(kind, world, K, mode):
         assert np.array_equal(got_lo, ref.lower) and np.array_equal(got_hi, ref.upper)
     finally:
         c.close()
+
+
+# ------------------------------------------------------------ field-pipelined heat CTMM
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_heat_pipelined_final_box(mode):
+    """heat3d CTMM with only the final box and n >= 2^22 takes the field-
+    pipelined driver (engine.cu run_heat_mm_pipelined: lower field integrated
+    while the upper field uploads, lower field downloaded while the upper one
+    integrates).  Same result as the oracle: bit-exact / within tolerance."""
+    g = 170  # n = 4.913e6
+    n = g ** 3
+    rng = np.random.default_rng(11)
+    lo = rng.uniform(0.5, 1.0, n)
+    hi = lo + rng.uniform(0.0, 0.5, n)
+    h = 0.2 / (g - 1) ** 2
+    m, prob = heat_problem(g, t1=3 * h, h=h, stride=0, lo=lo, hi=hi)
+    c = pk.Context(0, mode)
+    try:
+        tube = pk.mixed_monotonicity(prob, ctx=c)
+        ref = oracle_for("mm", prob)
+        if mode == "exact":
+            assert_bitexact(tube, ref)
+        else:
+            assert_within(tube, ref)
+        bad = lo.copy()
+        bad[12345] = hi[12345] + 1.0
+        prob2 = pk.ReachProblem(m, pk.IntervalVector(bad, hi, validate=False), None, 0.0, 3 * h, h, 0)
+        with pytest.raises(ValueError, match="lower > upper at component 12345"):
+            pk.mixed_monotonicity(prob2, ctx=c)
+    finally:
+        c.close()
