@@ -239,14 +239,14 @@ constexpr int kCwSeg = 32 * kCwP;            // loaded per warp
 constexpr int kCwOut = kCwSeg - 2 * kChainHalo;  // 120 outputs per warp
 constexpr int kCwWarps = 8;
 #ifndef PIRK_CW_MINB
-#define PIRK_CW_MINB 3  // 3 CTAs (24 warps) per SM: measured fastest (n=1e7 traffic 0.111 vs 0.132 ms at 1)
+#define PIRK_CW_MINB 3  // CTAs per SM: 3 for the chain (4 spills), 4 for traffic (n=1e7: 0.0914 vs 0.0968 ms)
 #endif
 #ifndef PIRK_CW_VEC
 #define PIRK_CW_VEC 1
 #endif
 
 template <bool Exact, int Kind, int Method>
-__global__ void __launch_bounds__(32 * kCwWarps, PIRK_CW_MINB)
+__global__ void __launch_bounds__(32 * kCwWarps, (Kind == kKindTraffic && PIRK_CW_MINB == 3) ? 4 : PIRK_CW_MINB)
 chain_warp_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc,
                   const unsigned long long step, unsigned long long* __restrict__ fail) {
     (void)sizeof(ModeCheck<Exact>);
