@@ -222,7 +222,9 @@ def heat_e2e(args, pk, torch, world):
            "n": n, "grid": g, "api": "paper_2001_10635_b200.mixed_monotonicity",
            "step": "one full C5 reach call (H2D initial box, 100 RK4 steps, order check, D2H final box); "
                    "lower field integrated while the upper field uploads, downloaded while it integrates",
-           "warmup_calls": 1}
+           "warmup_calls": 1,
+           "phases_s": {"setup": tube.report.phases.setup_s,
+                        "integration_incl_transfers": tube.report.phases.integration_s}}
     ok = bool(np.isfinite(olo[:: max(1, n // 4096)]).all())
     del tube, prob, lo, hi, olo, ohi
     for b in bufs:
