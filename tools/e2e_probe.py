@@ -14,7 +14,7 @@ ohi = torch.empty((1, n), dtype=torch.float64).pin_memory()
 ctx = pk.Context(0, "fast")
 prob = pk.ReachProblem(pk.make_heat3d(g), pk.IntervalVector(lo.numpy(), hi.numpy(), validate=False), None,
                        0.0, 100 * 5e-8, 5e-8, 0)
-for r in range(2):
+for r in range(int(os.environ.get("REPS", "2"))):
     t = time.perf_counter()
     tube = pk.mixed_monotonicity(prob, ctx=ctx, out=(olo.numpy(), ohi.numpy()))
     dt = time.perf_counter() - t
