@@ -245,17 +245,23 @@ constexpr int kCwWarps = 8;
 #define PIRK_CW_VEC 1
 #endif
 
-template <bool Exact, int Kind, int Method>
+// S RK4 steps per launch (S = 2: temporal blocking for full-domain runs; the
+// segment keeps 128 - 8S outputs, the halo grows to 4S per side, each step's
+// non-finite values are recorded under their own step index).
+template <int S>
+constexpr int cw_out() { return kCwSeg - 2 * kChainHalo * S; }
+
+template <bool Exact, int Kind, int Method, int S = 1>
 __global__ void __launch_bounds__(32 * kCwWarps, (Kind == kKindTraffic && PIRK_CW_MINB == 3) ? 4 : PIRK_CW_MINB)
-chain_warp_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc,
+chain_warp_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc0, const StepConsts sc1,
                   const unsigned long long step, unsigned long long* __restrict__ fail) {
     (void)sizeof(ModeCheck<Exact>);
     const int lane = threadIdx.x & 31;
     const long long n = static_cast<long long>(m.n);
     const long long seg = static_cast<long long>(w.out_begin) +
-                          (static_cast<long long>(blockIdx.x) * kCwWarps + (threadIdx.x >> 5)) * kCwOut -
-                          kChainHalo;
-    if (seg + kChainHalo >= static_cast<long long>(w.out_end)) return;  // whole warp: uniform
+                          (static_cast<long long>(blockIdx.x) * kCwWarps + (threadIdx.x >> 5)) * cw_out<S>() -
+                          kChainHalo * S;
+    if (seg + kChainHalo * S >= static_cast<long long>(w.out_end)) return;  // whole warp: uniform
     const long long g0 = seg + kCwP * lane;  // global index of this lane's first component
     const long long wb = static_cast<long long>(w.win_begin), we = static_cast<long long>(w.win_end);
 
@@ -297,7 +303,7 @@ chain_warp_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc,
     const unsigned full = 0xffffffffu;
     // The boundary flags matter only in the (at most two) warps holding
     // component 0 or n-1: every other warp runs the stages without them.
-    auto stages = [&](auto edge_tag) {
+    auto stages = [&](auto edge_tag, const StepConsts& sc) {
     constexpr bool Edge = decltype(edge_tag)::value;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
@@ -388,32 +394,81 @@ chain_warp_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc,
         }
     }
     };
-    if (__any_sync(full, (first | last) != 0))
-        stages(std::true_type{});
-    else
-        stages(std::false_type{});
-
-    // ---- store the segment's outputs (lanes 1..30) and flag non-finite values
-    if (lane == 0 || lane == 31) return;
-#pragma unroll
-    for (int k = 0; k < kCwP; ++k) {
+    const bool edge = __any_sync(full, (first | last) != 0);
+    // a component this warp outputs (the others are halo, owned by a neighbour)
+    auto owned = [&](int k) {
+        const int e = kCwP * lane + k;
         const long long g = g0 + k;
-        if (g < static_cast<long long>(w.out_begin) || g >= static_cast<long long>(w.out_end)) continue;
-        const long long o = g - static_cast<long long>(w.out_begin);
-        w.out0[o] = x0[k];
-        w.out1[o] = x1[k];
-        if (!finite_d(x0[k]) || !finite_d(x1[k])) {
-            if constexpr (Method == kMethodMM) {
-                const unsigned long long comp =
-                    finite_d(x0[k]) ? static_cast<unsigned long long>(g) + static_cast<unsigned long long>(n)
-                                    : static_cast<unsigned long long>(g);
-                record_fail(fail, step, comp);
-            } else {
-                if (!finite_d(x0[k])) record_fail(fail, step, static_cast<unsigned long long>(g));
-                if (!finite_d(x1[k]) && fail) record_fail(fail + 1, step, static_cast<unsigned long long>(g));
+        return e >= kChainHalo * S && e < kCwSeg - kChainHalo * S && g >= static_cast<long long>(w.out_begin) &&
+               g < static_cast<long long>(w.out_end);
+    };
+    auto flag = [&](int k, unsigned long long at) {  // rk4.cpp:72-75 key: (step, component)
+        const long long g = g0 + k;
+        if constexpr (Method == kMethodMM) {
+            const unsigned long long comp =
+                finite_d(x0[k]) ? static_cast<unsigned long long>(g) + static_cast<unsigned long long>(n)
+                                : static_cast<unsigned long long>(g);
+            record_fail(fail, at, comp);
+        } else {
+            if (!finite_d(x0[k])) record_fail(fail, at, static_cast<unsigned long long>(g));
+            if (!finite_d(x1[k]) && fail) record_fail(fail + 1, at, static_cast<unsigned long long>(g));
+        }
+    };
+#pragma unroll
+    for (int st = 0; st < S; ++st) {
+        const StepConsts& sc = st == 0 ? sc0 : sc1;
+        if (edge)
+            stages(std::true_type{}, sc);
+        else
+            stages(std::false_type{}, sc);
+        if (st + 1 < S) {  // intermediate state: flag it under its own step, restart the stages
+#pragma unroll
+            for (int k = 0; k < kCwP; ++k) {
+                if (owned(k) && (!finite_d(x0[k]) || !finite_d(x1[k]))) flag(k, step + st);
+                u0[k] = x0[k];
+                u1[k] = x1[k];
+                acc0[k] = acc1[k] = 0.0;
             }
         }
     }
+
+    // ---- store the segment's outputs and flag non-finite values
+#pragma unroll
+    for (int k = 0; k < kCwP; ++k) {
+        if (!owned(k)) continue;
+        const long long g = g0 + k;
+        const long long o = g - static_cast<long long>(w.out_begin);
+        w.out0[o] = x0[k];
+        w.out1[o] = x1[k];
+        if (!finite_d(x0[k]) || !finite_d(x1[k])) flag(k, step + S - 1);
+    }
+}
+
+template <bool Exact, int S>
+cudaError_t launch_chain_warp(const ChainModel& m, const WindowArgs& w, const StepConsts& sc0,
+                              const StepConsts& sc1, unsigned long long step, unsigned long long* fail,
+                              cudaStream_t stream) {
+    const uint64_t count = w.out_end - w.out_begin;
+    const uint64_t per_block = static_cast<uint64_t>(kCwWarps) * cw_out<S>();
+    dim3 wgrid(static_cast<unsigned>((count + per_block - 1) / per_block)), wblock(32 * kCwWarps);
+    if (m.kind == kKindTraffic && m.method == kMethodMM)
+        chain_warp_kernel<Exact, kKindTraffic, kMethodMM, S><<<wgrid, wblock, 0, stream>>>(m, w, sc0, sc1, step, fail);
+    else if (m.kind == kKindTraffic && m.method == kMethodGB)
+        chain_warp_kernel<Exact, kKindTraffic, kMethodGB, S><<<wgrid, wblock, 0, stream>>>(m, w, sc0, sc1, step, fail);
+    else if (m.kind == kKindChain && m.method == kMethodMM)
+        chain_warp_kernel<Exact, kKindChain, kMethodMM, S><<<wgrid, wblock, 0, stream>>>(m, w, sc0, sc1, step, fail);
+    else
+        return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
+// Two RK4 steps in one launch (full-domain engine runs; temporal blocking).
+template <bool Exact>
+cudaError_t launch_chain_step2(const ChainModel& m, const WindowArgs& w, const StepConsts& sc0,
+                               const StepConsts& sc1, unsigned long long step, unsigned long long* fail,
+                               cudaStream_t stream) {
+    if (w.out_end <= w.out_begin) return cudaSuccess;
+    return launch_chain_warp<Exact, 2>(m, w, sc0, sc1, step, fail, stream);
 }
 
 template <bool Exact>
@@ -430,19 +485,7 @@ cudaError_t launch_chain_step(const ChainModel& m, const WindowArgs& w, const St
         const char* v = std::getenv("PIRK_CHAIN_KERNEL");
         return v && std::strcmp(v, "smem") == 0;
     }();
-    if (!use_smem) {
-        const uint64_t per_block = static_cast<uint64_t>(kCwWarps) * kCwOut;
-        dim3 wgrid(static_cast<unsigned>((count + per_block - 1) / per_block)), wblock(32 * kCwWarps);
-        if (m.kind == kKindTraffic && m.method == kMethodMM)
-            chain_warp_kernel<Exact, kKindTraffic, kMethodMM><<<wgrid, wblock, 0, stream>>>(m, w, sc, step, fail);
-        else if (m.kind == kKindTraffic && m.method == kMethodGB)
-            chain_warp_kernel<Exact, kKindTraffic, kMethodGB><<<wgrid, wblock, 0, stream>>>(m, w, sc, step, fail);
-        else if (m.kind == kKindChain && m.method == kMethodMM)
-            chain_warp_kernel<Exact, kKindChain, kMethodMM><<<wgrid, wblock, 0, stream>>>(m, w, sc, step, fail);
-        else
-            return cudaErrorInvalidValue;
-        return cudaGetLastError();
-    }
+    if (!use_smem) return launch_chain_warp<Exact, 1>(m, w, sc, sc, step, fail, stream);
     const unsigned int blocks = static_cast<unsigned int>((count + kChainTile - 1) / kChainTile);
     dim3 grid(blocks), block(kChainThreads);
     if (m.kind == kKindTraffic && m.method == kMethodMM)

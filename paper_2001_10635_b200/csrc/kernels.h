@@ -55,6 +55,12 @@ cudaError_t launch_chain_step(const ChainModel& m, const WindowArgs& w, const St
                               unsigned long long step, unsigned long long* fail,
                               cudaStream_t stream);
 
+// Two chain steps per launch (step, step+1) with the warp-tiled kernel.
+template <bool Exact>
+cudaError_t launch_chain_step2(const ChainModel& m, const WindowArgs& w, const StepConsts& sc0,
+                               const StepConsts& sc1, unsigned long long step, unsigned long long* fail,
+                               cudaStream_t stream);
+
 template <bool Exact>
 cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const StepConsts& sc,
                              unsigned long long step, unsigned long long* fail,

@@ -148,13 +148,16 @@ def test_heat_block_variants(variant):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("variant", ["smem", "warp"])
+@pytest.mark.parametrize("variant", ["smem", "warp", "warp_single_step"])
 def test_chain_kernel_variants(variant):
-    """Both chain kernels in both modes (defaults: warp-tiled in fast mode,
-    shared-memory tiles in exact mode) on the traffic and coupled-chain tests."""
+    """The chain kernels in both modes on the traffic and coupled-chain tests:
+    shared-memory tiles, the warp-tiled kernel (default: two RK4 steps per
+    launch in full-domain runs) and the warp-tiled kernel one step at a time."""
     import os, subprocess, sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PIRK_CHAIN_KERNEL=variant)
+    env = dict(os.environ, PIRK_CHAIN_KERNEL=variant.split("_")[0])
+    if variant == "warp_single_step":
+        env["PIRK_CHAIN_FUSE"] = "0"
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
                         os.path.join(root, "tests", "test_gpu_parity.py"),
                         "-k", "(traffic or chain) and not variant"],
