@@ -253,7 +253,7 @@ constexpr int cw_out() { return kCwSeg - 2 * kChainHalo * S; }
 
 template <bool Exact, int Kind, int Method, int S = 1>
 __global__ void __launch_bounds__(32 * kCwWarps, (Kind == kKindTraffic && PIRK_CW_MINB == 3) ? 4 : PIRK_CW_MINB)
-chain_warp_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc0, const StepConsts sc1,
+chain_warp_kernel(const ChainModel m, const WindowArgs w, const StepConstsN scs,
                   const unsigned long long step, unsigned long long* __restrict__ fail) {
     (void)sizeof(ModeCheck<Exact>);
     const int lane = threadIdx.x & 31;
@@ -416,7 +416,7 @@ chain_warp_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc0, 
     };
 #pragma unroll
     for (int st = 0; st < S; ++st) {
-        const StepConsts& sc = st == 0 ? sc0 : sc1;
+        const StepConsts& sc = scs.s[st];
         if (edge)
             stages(std::true_type{}, sc);
         else
@@ -445,30 +445,33 @@ chain_warp_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc0, 
 }
 
 template <bool Exact, int S>
-cudaError_t launch_chain_warp(const ChainModel& m, const WindowArgs& w, const StepConsts& sc0,
-                              const StepConsts& sc1, unsigned long long step, unsigned long long* fail,
-                              cudaStream_t stream) {
+cudaError_t launch_chain_warp(const ChainModel& m, const WindowArgs& w, const StepConstsN& scs,
+                              unsigned long long step, unsigned long long* fail, cudaStream_t stream) {
     const uint64_t count = w.out_end - w.out_begin;
     const uint64_t per_block = static_cast<uint64_t>(kCwWarps) * cw_out<S>();
     dim3 wgrid(static_cast<unsigned>((count + per_block - 1) / per_block)), wblock(32 * kCwWarps);
     if (m.kind == kKindTraffic && m.method == kMethodMM)
-        chain_warp_kernel<Exact, kKindTraffic, kMethodMM, S><<<wgrid, wblock, 0, stream>>>(m, w, sc0, sc1, step, fail);
+        chain_warp_kernel<Exact, kKindTraffic, kMethodMM, S><<<wgrid, wblock, 0, stream>>>(m, w, scs, step, fail);
     else if (m.kind == kKindTraffic && m.method == kMethodGB)
-        chain_warp_kernel<Exact, kKindTraffic, kMethodGB, S><<<wgrid, wblock, 0, stream>>>(m, w, sc0, sc1, step, fail);
+        chain_warp_kernel<Exact, kKindTraffic, kMethodGB, S><<<wgrid, wblock, 0, stream>>>(m, w, scs, step, fail);
     else if (m.kind == kKindChain && m.method == kMethodMM)
-        chain_warp_kernel<Exact, kKindChain, kMethodMM, S><<<wgrid, wblock, 0, stream>>>(m, w, sc0, sc1, step, fail);
+        chain_warp_kernel<Exact, kKindChain, kMethodMM, S><<<wgrid, wblock, 0, stream>>>(m, w, scs, step, fail);
     else
         return cudaErrorInvalidValue;
     return cudaGetLastError();
 }
 
-// Two RK4 steps in one launch (full-domain engine runs; temporal blocking).
+// S = 2..4 RK4 steps in one launch (full-domain engine runs; temporal blocking).
 template <bool Exact>
-cudaError_t launch_chain_step2(const ChainModel& m, const WindowArgs& w, const StepConsts& sc0,
-                               const StepConsts& sc1, unsigned long long step, unsigned long long* fail,
-                               cudaStream_t stream) {
+cudaError_t launch_chain_steps(const ChainModel& m, const WindowArgs& w, const StepConstsN& scs, int S,
+                               unsigned long long step, unsigned long long* fail, cudaStream_t stream) {
     if (w.out_end <= w.out_begin) return cudaSuccess;
-    return launch_chain_warp<Exact, 2>(m, w, sc0, sc1, step, fail, stream);
+    switch (S) {
+        case 2: return launch_chain_warp<Exact, 2>(m, w, scs, step, fail, stream);
+        case 3: return launch_chain_warp<Exact, 3>(m, w, scs, step, fail, stream);
+        case 4: return launch_chain_warp<Exact, 4>(m, w, scs, step, fail, stream);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 template <bool Exact>
@@ -485,7 +488,11 @@ cudaError_t launch_chain_step(const ChainModel& m, const WindowArgs& w, const St
         const char* v = std::getenv("PIRK_CHAIN_KERNEL");
         return v && std::strcmp(v, "smem") == 0;
     }();
-    if (!use_smem) return launch_chain_warp<Exact, 1>(m, w, sc, sc, step, fail, stream);
+    if (!use_smem) {
+        StepConstsN one;
+        one.s[0] = sc;
+        return launch_chain_warp<Exact, 1>(m, w, one, step, fail, stream);
+    }
     const unsigned int blocks = static_cast<unsigned int>((count + kChainTile - 1) / kChainTile);
     dim3 grid(blocks), block(kChainThreads);
     if (m.kind == kKindTraffic && m.method == kMethodMM)

@@ -112,6 +112,14 @@ StepConsts host_step(double t0, double t1, double h, uint64_t k, uint64_t total)
 bool is_chain(const pirk_model* m) { return m->kind == PIRK_TRAFFIC || m->kind == PIRK_CHAIN; }
 bool is_heat(const pirk_model* m) { return m->kind == PIRK_HEAT3D; }
 
+#ifndef PIRK_CHAIN_FUSE_DEFAULT
+// RK4 steps per chain launch in full-domain runs.  Measured (ms per step,
+// S = 2 / 3 / 4): fast traffic n=1e6 0.0096 / 0.0111 / 0.0102, n=1e7 0.068 /
+// 0.066 / 0.069; fast chain n=1e7 0.087 / 0.082 / 0.086; exact chain 0.144 /
+// 0.153 / 0.167.
+#define PIRK_CHAIN_FUSE_DEFAULT 2
+#endif
+
 // Descriptor consistency (the reference's make_* constructors enforce these,
 // models.cpp:47-53, 92-97, and fix dim/input_dim per model).
 bool check_model(pirk_ctx* ctx, const pirk_model* m, pirk_status& st) {
@@ -452,13 +460,16 @@ pirk_status engine_init(pirk_ctx* ctx, const pirk_model* m, int method, const pi
 // Full-domain chain runs advance two RK4 steps per launch (chain_warp_kernel
 // with S = 2: twice the halo, half the HBM round trips).  PIRK_CHAIN_FUSE=0 or
 // PIRK_CHAIN_KERNEL=smem keep one step per launch.
-bool chain_fuse_enabled() {
-    static const bool on = [] {
+int chain_fuse_steps() {  // PIRK_CHAIN_FUSE=0|1 (off), 2..4
+    static const int v = [] {
         const char* f = std::getenv("PIRK_CHAIN_FUSE");
         const char* k = std::getenv("PIRK_CHAIN_KERNEL");
-        return !(f && std::strcmp(f, "0") == 0) && !(k && std::strcmp(k, "smem") == 0);
+        if (k && std::strcmp(k, "smem") == 0) return 1;
+        if (!f) return PIRK_CHAIN_FUSE_DEFAULT;
+        const int n = std::atoi(f);
+        return n < 1 ? 1 : (n > 4 ? 4 : n);
     }();
-    return on;
+    return v;
 }
 
 pirk_status engine_advance(pirk_engine* e, uint64_t nsteps) {
@@ -467,19 +478,21 @@ pirk_status engine_advance(pirk_engine* e, uint64_t nsteps) {
     // measured (n = 1e7, ms per step, 1 vs 2 steps per launch): fast traffic
     // 0.092 -> 0.067, fast chain 0.099 -> 0.087, exact chain 0.153 -> 0.144;
     // exact traffic 0.158 -> 0.165 (register pressure), so it stays at one
-    const bool fuse = is_chain(&e->model) && chain_fuse_enabled() &&
-                      (!exact_mode(ctx) || e->model.kind == PIRK_CHAIN);
-    while (fuse && left >= 2 && e->done + 2 <= e->plan.total) {
+    const int S = (is_chain(&e->model) && (!exact_mode(ctx) || e->model.kind == PIRK_CHAIN)) ? chain_fuse_steps() : 1;
+    while (S >= 2 && left >= 2 && e->done + 2 <= e->plan.total) {
         const uint64_t k = e->done;
-        const StepConsts sc0 = host_step(e->t0, e->t1, e->h, k, e->plan.total);
-        const StepConsts sc1 = host_step(e->t0, e->t1, e->h, k + 1, e->plan.total);
+        int s_now = S;
+        while (s_now > left || e->done + s_now > e->plan.total) --s_now;
+        if (s_now < 2) break;
+        StepConstsN scs;
+        for (int q = 0; q < s_now; ++q) scs.s[q] = host_step(e->t0, e->t1, e->h, k + q, e->plan.total);
         WindowArgs w{e->s0(), e->s1(), e->o0(), e->o1(), 0, e->units, 0, e->units};
         ctx->launches++;
-        CK(ctx, exact_mode(ctx) ? launch_chain_step2<true>(e->cm, w, sc0, sc1, k, e->d_fail.p, ctx->stream)
-                                : launch_chain_step2<false>(e->cm, w, sc0, sc1, k, e->d_fail.p, ctx->stream));
+        CK(ctx, exact_mode(ctx) ? launch_chain_steps<true>(e->cm, w, scs, s_now, k, e->d_fail.p, ctx->stream)
+                                : launch_chain_steps<false>(e->cm, w, scs, s_now, k, e->d_fail.p, ctx->stream));
         e->cur ^= 1;
-        e->done += 2;
-        left -= 2;
+        e->done += s_now;
+        left -= s_now;
     }
     for (uint64_t i = 0; i < left && e->done < e->plan.total; ++i) {
         const uint64_t k = e->done;

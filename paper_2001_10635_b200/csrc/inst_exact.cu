@@ -9,9 +9,8 @@ namespace pirk {
 template cudaError_t launch_chain_step<true>(const ChainModel&, const WindowArgs&,
                                              const StepConsts&, unsigned long long,
                                              unsigned long long*, cudaStream_t);
-template cudaError_t launch_chain_step2<true>(const ChainModel&, const WindowArgs&, const StepConsts&,
-                                                const StepConsts&, unsigned long long, unsigned long long*,
-                                                cudaStream_t);
+template cudaError_t launch_chain_steps<true>(const ChainModel&, const WindowArgs&, const StepConstsN&, int,
+                                                unsigned long long, unsigned long long*, cudaStream_t);
 template cudaError_t launch_heat_step<true>(const HeatModel&, const WindowArgs&,
                                             const StepConsts&, unsigned long long,
                                             unsigned long long*, cudaStream_t, int);

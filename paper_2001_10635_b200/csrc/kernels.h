@@ -55,11 +55,13 @@ cudaError_t launch_chain_step(const ChainModel& m, const WindowArgs& w, const St
                               unsigned long long step, unsigned long long* fail,
                               cudaStream_t stream);
 
-// Two chain steps per launch (step, step+1) with the warp-tiled kernel.
+// S (2..4) chain steps per launch (step .. step+S-1) with the warp-tiled kernel.
+struct StepConstsN {
+    StepConsts s[4];
+};
 template <bool Exact>
-cudaError_t launch_chain_step2(const ChainModel& m, const WindowArgs& w, const StepConsts& sc0,
-                               const StepConsts& sc1, unsigned long long step, unsigned long long* fail,
-                               cudaStream_t stream);
+cudaError_t launch_chain_steps(const ChainModel& m, const WindowArgs& w, const StepConstsN& scs, int S,
+                               unsigned long long step, unsigned long long* fail, cudaStream_t stream);
 
 template <bool Exact>
 cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const StepConsts& sc,
