@@ -363,8 +363,11 @@ __device__ void hull_fold(const double* x, bool active, int n, unsigned long lon
     __syncthreads();
 }
 
+#ifndef PIRK_MC_MINB
+#define PIRK_MC_MINB 4  // 16 warps/SM: arch-quad fast m=1e6 5.62 vs 5.91 ms at 1 (5: 5.60)
+#endif
 template <bool Exact, int N>
-__global__ void __launch_bounds__(kMcThreads)
+__global__ void __launch_bounds__(kMcThreads, PIRK_MC_MINB)
 monte_carlo_kernel(const SmallModel m, const McArgs a) {
     (void)sizeof(ModeCheck<Exact>);
     constexpr int NA = (N > 0) ? N : kSmallMax;
