@@ -234,7 +234,10 @@ chain_step_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc,
 // the outputs).  No shared memory and no barriers: 16 B of HBM traffic per
 // state-update plus 8 halo loads per 120 outputs.  Per-component arithmetic
 // is the expression-for-expression restatement of chain_step_kernel above.
-constexpr int kCwP = 4;                      // components per lane
+#ifndef PIRK_CW_P
+#define PIRK_CW_P 4  // 8 per lane measured slower (n=1e7 chain 0.092 ms at 2 CTAs/SM vs 0.087)
+#endif
+constexpr int kCwP = PIRK_CW_P;              // components per lane
 constexpr int kCwSeg = 32 * kCwP;            // loaded per warp
 constexpr int kCwOut = kCwSeg - 2 * kChainHalo;  // 120 outputs per warp
 constexpr int kCwWarps = 8;
