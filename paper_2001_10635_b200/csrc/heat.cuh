@@ -122,6 +122,9 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned b
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
     asm volatile(
         "{\n .reg .pred p;\nPIRK_WAIT_%=:\n"
