@@ -64,6 +64,18 @@
 #ifndef PIRK_STRIP_SPLITBAR
 #define PIRK_STRIP_SPLITBAR 1  // split per-plane barrier (mbarrier arrive at the end, wait before the first publish): 38.2 -> 35.1 ms at g=1600
 #endif
+#ifndef PIRK_STRIP_XSWAP
+#define PIRK_STRIP_XSWAP 1  // x(j-1) to TMEM from stage 1, A4 formed in stage 3: 35.0 -> 34.9 ms
+#endif
+#ifndef PIRK_STRIP_XCARRY
+#define PIRK_STRIP_XCARRY 0  // x(j) kept in registers as the next centre: 36.9 vs 34.9 ms (pressure)
+#endif
+#ifndef PIRK_STRIP_LADDER
+#define PIRK_STRIP_LADDER 0  // 1/2: per-level publish barriers (2: TMA after stage 3): 37.1 / 37.3 vs 35.0 ms at g=1600
+#endif
+#if PIRK_STRIP_LADDER && !PIRK_STRIP_SPLITBAR
+#error "PIRK_STRIP_LADDER needs PIRK_STRIP_SPLITBAR"
+#endif
 #ifndef PIRK_STRIP_S4SKIP
 #define PIRK_STRIP_S4SKIP 0  // halo warps 0 and 15 skip stage 4 (measured slower: 7.40 vs 6.55 ms, g=800)
 #endif
@@ -131,6 +143,7 @@ struct HeatStrip {
     unsigned tt;  // TMEM address of slot 0
     int xs;       // x ring slot of plane j
     int xph;      // mbarrier phase bit per slot
+    double xc[8];  // XCARRY: own block of x(j) for the next iteration (valid after any iteration)
 
     __device__ __forceinline__ unsigned ts(int slot) const { return tt + 16u * slot; }
     __device__ __forceinline__ double* xslot(int s) const { return XR + s * kSXSlot; }
@@ -264,12 +277,20 @@ struct HeatStrip {
         const double* Xj = xslot(xs);
         const double* Xm = xslot((xs + 3) & 3);  // x(j-1)
         // split barrier: the previous plane's arrivals (completion j-1-zs)
-        auto wait_prev = [&]() {
-            if (PIRK_STRIP_SPLITBAR && j > zs) mbar_wait(done, static_cast<unsigned>(j - 1 - zs) & 1u);
+        // (ladder: done[1] / done[2] complete when every warp has published
+        // level 1 / level 2 of a plane, so a fast warp waits only for the
+        // exchange rows it is about to overwrite)
+        auto wait_bar = [&](int b) {
+            if (PIRK_STRIP_SPLITBAR && j > zs) mbar_wait(done + b, static_cast<unsigned>(j - 1 - zs) & 1u);
+        };
+        auto wait_prev = [&]() { wait_bar(PIRK_STRIP_LADDER ? 1 : 0); };
+        auto arrive = [&](int b) {
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) mbar_arrive(done + b);
         };
         if (has_x) {  // issue first: a late x(j) must not delay the prefetch behind it
-            if (threadIdx.x == 0 && (!edge || j + 2 < ze)) {
-                wait_prev();  // the target slot (x(j-2)) was read in the previous iteration
+            if (PIRK_STRIP_LADDER < 2 && threadIdx.x == 0 && (!edge || j + 2 < ze)) {
+                wait_bar(0);  // the target slot (x(j-2)) was read in the previous iteration
                 tma(j + 2, (xs + 2) & 3);
             }
             if (PIRK_STRIP_L2PF > 0 && threadIdx.x == 0 && j + 2 + PIRK_STRIP_L2PF < ze)
@@ -279,15 +300,29 @@ struct HeatStrip {
 
         // ---- stage 1 at p = j-1: centre and base x(j-1), z- x(j-2), z+ x(j)
         double o1[8], zm2[8];
+        double xb[8];  // XSWAP: x(j-3), the base of stage 3, read before x(j-1) replaces it
         if (v1) {
             double C[8], zm[8], zp[8], T[2], B[2];
-            own_x(Xm, C);
+            if (PIRK_STRIP_XCARRY && !edge) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) C[i] = xc[i];
+            } else {
+                own_x(Xm, C);
+            }
+            if constexpr (PIRK_STRIP_XSWAP) {
+                tm_ld8(ts(XB), xb);
+                st8(ts(XB), C);  // x(j-1) replaces x(j-3)
+            }
             tm_ld8x2(ts(XA), ts(U1B), zm, zm2);  // x(j-2); u1(j-3) before it is overwritten
             if (!edge || j < g) {
                 own_x(Xj, zp);
             } else {  // x(g) := x(g-1)
 #pragma unroll
                 for (int i = 0; i < 8; ++i) zp[i] = C[i];
+            }
+            if constexpr (PIRK_STRIP_XCARRY) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) xc[i] = zp[i];  // (beyond g only edge iterations follow)
             }
             if (edge && j - 1 == 0) {  // x(-1) := x(0)
 #pragma unroll
@@ -299,6 +334,13 @@ struct HeatStrip {
             wait_prev();  // every warp is past the previous plane's exchange reads
             publish(PH, 0, o1);
         } else {
+            if constexpr (PIRK_STRIP_XSWAP) {
+                double w[8];
+                tm_ld8(ts(XB), xb);
+                own_x(Xm, w);
+                st8(ts(XB), w);
+            }
+            if (PIRK_STRIP_XCARRY && has_x) own_x(Xj, xc);  // (only edge iterations get here)
             wait_prev();
             if (v2) tm_ld8(ts(U1B), zm2);
         }
@@ -319,17 +361,26 @@ struct HeatStrip {
             u_tb(PH ^ 1, 0, T, B);
             stage(C, T, B, zm2, o1, bs, hp.hn[1], o2);
             st8(ts(U2B), o2);  // u2(j-2) replaces u2(j-4)
+            if (PIRK_STRIP_LADDER) wait_bar(2);
             publish(PH, 1, o2);
-        } else if (v3) {
-            tm_ld8(ts(U2B), zm3);
+        } else {
+            if (PIRK_STRIP_LADDER) wait_bar(2);
+            if (v3) tm_ld8(ts(U2B), zm3);
         }
+        if (PIRK_STRIP_LADDER) arrive(1);
         // ---- stage 3 at p = j-3: centre u2(j-3), z- u2(j-4), z+ u2(j-2), base x(j-3)
-        double o3[8], C4[8];
+        double o3[8], C4[8], av[8];
         const bool s4 = (v4 || a4) && inner;     // halo warps 0 and 15 never run stage 4
         if (s4) tm_ld8(ts(kSU3), C4);  // u3(j-4) before it is overwritten
         if (v3) {
             double C[8], bs[8], T[2], B[2];
-            tm_ld8x2(ts(U2A), ts(XB), C, bs);
+            if constexpr (PIRK_STRIP_XSWAP) {
+                tm_ld8(ts(U2A), C);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) bs[i] = xb[i];
+            } else {
+                tm_ld8x2(ts(U2A), ts(XB), C, bs);
+            }
             if (edge && j - 3 == 0) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) zm3[i] = C[i];
@@ -341,18 +392,41 @@ struct HeatStrip {
             u_tb(PH ^ 1, 1, T, B);
             stage(C, T, B, zm3, o2, bs, hp.hn[2], o3);
             if (inner) st8(ts(kSU3), o3);  // u3(j-3) replaces u3(j-4)
+            if (PIRK_STRIP_LADDER) wait_bar(0);
             publish(PH, 2, o3);
+            if (PIRK_STRIP_XSWAP && s4) {  // A4(j-3) = x(j-3) + c4 (u3(j-4) - 6 u3(j-3)); A4(j-4) first
+                if (edge && j - 3 == 0) {  // u3(-1) := u3(0) (stage 4 does not run)
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) C4[i] = o3[i];
+                }
+                tm_ld8(ts(kSA4), av);
+                if (a4) {
+                    double an[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) an[i] = fma(hp.hn[3], fma(-6.0, o3[i], C4[i]), bs[i]);
+                    st8(ts(kSA4), an);
+                }
+            }
+        } else if (PIRK_STRIP_LADDER) {
+            wait_bar(0);
         }
+        if (PIRK_STRIP_LADDER == 2 && has_x && threadIdx.x == 0 && (!edge || j + 2 < ze))
+            tma(j + 2, (xs + 2) & 3);  // every warp is past the previous plane: its x slot is free
+        if (PIRK_STRIP_LADDER) arrive(2);
         // ---- stage 4 at p = j-4: y = A4(j-4) + c4 (inplane(u3(j-4)) + u3(j-3)) to
         // HBM; A4(j-3) = x(j-3) + c4 (u3(j-4) - 6 u3(j-3)); x(j-1) replaces x(j-3)
         if (s4) {
-            double av[8], x3[8];
-            tm_ld8x2(ts(kSA4), ts(XB), av, x3);
+            double x3[8];
+            if constexpr (PIRK_STRIP_XSWAP) {
+                if (!v3) tm_ld8(ts(kSA4), av);  // (a4 implies v3)
+            } else {
+                tm_ld8x2(ts(kSA4), ts(XB), av, x3);
+            }
             if (edge && j - 4 == g - 1) {  // u3(g) := u3(g-1) (stage 3 did not run)
 #pragma unroll
                 for (int i = 0; i < 8; ++i) o3[i] = C4[i];
             }
-            if (edge && j - 3 == 0) {  // u3(-1) := u3(0) (stage 4 does not run)
+            if (!PIRK_STRIP_XSWAP && edge && j - 3 == 0) {  // u3(-1) := u3(0) (stage 4 does not run)
 #pragma unroll
                 for (int i = 0; i < 8; ++i) C4[i] = o3[i];
             }
@@ -376,14 +450,14 @@ struct HeatStrip {
                     heat_strip_report(stp, g, g2, j - 4, gout, st_own ? 0xffu : st_mask, field, method, step,
                                       fail, n_total);
             }
-            if (a4) {
+            if (!PIRK_STRIP_XSWAP && a4) {
                 double an[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) an[i] = fma(hp.hn[3], fma(-6.0, o3[i], C4[i]), x3[i]);
                 st8(ts(kSA4), an);
             }
         }
-        {
+        if constexpr (!PIRK_STRIP_XSWAP) {
             double w[8];
             own_x(Xm, w);
             st8(ts(XB), w);  // x(j-1) replaces x(j-3)
@@ -396,8 +470,7 @@ struct HeatStrip {
         // one barrier per plane: this iteration's rows (buffer j & 1) become
         // readable, and the next iteration may overwrite buffer (j - 1) & 1
         if constexpr (PIRK_STRIP_SPLITBAR) {
-            __syncwarp();
-            if ((threadIdx.x & 31) == 0) mbar_arrive(done);
+            arrive(0);
         } else {
             __syncthreads();
         }
@@ -448,7 +521,7 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
     (void)sc;
     extern __shared__ __align__(128) double smem[];
     __shared__ __align__(8) unsigned long long bars[kSXSlots];
-    __shared__ __align__(8) unsigned long long done_bar;
+    __shared__ __align__(8) unsigned long long done_bar[3];
     __shared__ unsigned tmem_base;
     const int tid = threadIdx.x;
     const long long g = static_cast<long long>(m.g);
@@ -497,7 +570,7 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
     if (warp == 0) tmem_alloc512(&tmem_base);
     if (tid == 0) {
         for (int s = 0; s < kSXSlots; ++s) mbar_init(bars + s, 1);
-        mbar_init(&done_bar, kSThreads / 32);
+        for (int b = 0; b < 3; ++b) mbar_init(done_bar + b, kSThreads / 32);
         mbar_fence_init();
     }
     tmem_fence_before();
@@ -529,7 +602,7 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
         r.bx0 = static_cast<int>(ix0) - kHeatH, r.by0 = static_cast<int>(iy0) - kHeatH;              \
         r.wbz = static_cast<int>(w.win_begin);                                                       \
         r.bars = bars;                                                                               \
-        r.done = &done_bar;                                                                          \
+        r.done = done_bar;                                                                           \
         r.tt = tt;                                                                                   \
         r.run();                                                                                     \
     }
