@@ -35,6 +35,17 @@ struct pirk_ctx {
     uint64_t launches = 0;
     unsigned long long* d_flags = nullptr;  // scratch device flags [16]
     unsigned long long* h_flags = nullptr;  // pinned mirror
+    // state buffers of the last finished run, kept for the next run of the same
+    // size: freeing 4 x 32 GB costs up to ~0.5 s of unmapping per call
+    struct Block {
+        void* p;
+        size_t bytes;
+    };
+    std::vector<Block> cache;
+    void flush_cache() {
+        for (const Block& b : cache) cudaFree(b.p);
+        cache.clear();
+    }
 };
 
 namespace {
@@ -332,11 +343,44 @@ bool check_problem(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p, bo
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
-    ~DevBuf() { if (p) cudaFree(p); }
+    pirk_ctx* owner = nullptr;  // set: a state buffer that returns to owner->cache
+    size_t bytes = 0;
+    ~DevBuf() {
+        if (!p) return;
+        if (owner && owner->cache.size() < 8) {
+            owner->cache.push_back({p, bytes});
+        } else {
+            cudaFree(p);
+        }
+    }
     cudaError_t alloc(size_t count) { return cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T) + 16); }
+    // take a cached block of exactly this size, else drop the cache (it was sized
+    // for another problem) and allocate
+    cudaError_t alloc_state(pirk_ctx* ctx, size_t count) {
+        bytes = count * sizeof(T) + 16;
+        owner = ctx;
+        for (size_t i = 0; i < ctx->cache.size(); ++i) {
+            if (ctx->cache[i].bytes == bytes) {
+                p = static_cast<T*>(ctx->cache[i].p);
+                ctx->cache.erase(ctx->cache.begin() + static_cast<long>(i));
+                return cudaSuccess;
+            }
+        }
+        ctx->flush_cache();
+        return cudaMalloc(reinterpret_cast<void**>(&p), bytes);
+    }
 };
 
 bool exact_mode(const pirk_ctx* ctx) { return ctx->mode == PIRK_MODE_EXACT; }
+
+// PIRK_STATE_CACHE=0: free the state buffers after every run
+bool state_cache_on() {
+    static const bool on = [] {
+        const char* v = std::getenv("PIRK_STATE_CACHE");
+        return !(v && std::strcmp(v, "0") == 0);
+    }();
+    return on;
+}
 
 cudaError_t step_launch(pirk_ctx* ctx, const pirk_model* m, int method, const ChainModel& cm,
                         const HeatModel& hm, const WindowArgs& w, const StepConsts& sc,
@@ -386,6 +430,7 @@ struct pirk_engine {
     uint64_t n = 0, units = 0, unit = 1;
     DevBuf<double> a0, a1, b0, b1;
     int cur = 0;               // 0: state in (a0,a1); 1: in (b0,b1)
+    bool cache_state = false;  // one-shot runs: state buffers go back to ctx->cache
     uint64_t done = 0;
     DevBuf<unsigned long long> d_fail;  // [2]
     ChainModel cm{};
@@ -427,10 +472,17 @@ pirk_status engine_init(pirk_ctx* ctx, const pirk_model* m, int method, const pi
     e->cm = chain_model(m, method, p0, p1);
     e->hm = heat_model(m, method);
     const size_t n = e->n;
-    CK(ctx, e->a0.alloc(n));
-    CK(ctx, e->a1.alloc(n));
-    CK(ctx, e->b0.alloc(n));
-    CK(ctx, e->b1.alloc(n));
+    if (e->cache_state && state_cache_on()) {
+        CK(ctx, e->a0.alloc_state(ctx, n));
+        CK(ctx, e->a1.alloc_state(ctx, n));
+        CK(ctx, e->b0.alloc_state(ctx, n));
+        CK(ctx, e->b1.alloc_state(ctx, n));
+    } else {
+        CK(ctx, e->a0.alloc(n));
+        CK(ctx, e->a1.alloc(n));
+        CK(ctx, e->b0.alloc(n));
+        CK(ctx, e->b1.alloc(n));
+    }
     CK(ctx, e->d_fail.alloc(2));
     CK(ctx, cudaMemsetAsync(e->d_fail.p, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
     CK(ctx, cudaMemcpyAsync(e->a0.p, p->init_lower, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
@@ -556,10 +608,11 @@ pirk_status run_heat_mm_pipelined(pirk_ctx* ctx, const pirk_model* m, const pirk
         return fail(ctx, PIRK_EINVAL, "dimension exceeds the device failure-key range");
     e.hm = heat_model(m, PIRK_METHOD_MM);
     const size_t n = e.n;
-    CK(ctx, e.a0.alloc(n));
-    CK(ctx, e.a1.alloc(n));
-    CK(ctx, e.b0.alloc(n));
-    CK(ctx, e.b1.alloc(n));
+    const bool cache = state_cache_on();
+    CK(ctx, cache ? e.a0.alloc_state(ctx, n) : e.a0.alloc(n));
+    CK(ctx, cache ? e.a1.alloc_state(ctx, n) : e.a1.alloc(n));
+    CK(ctx, cache ? e.b0.alloc_state(ctx, n) : e.b0.alloc(n));
+    CK(ctx, cache ? e.b1.alloc_state(ctx, n) : e.b1.alloc(n));
     CK(ctx, e.d_fail.alloc(2));
     DevBuf<unsigned long long> flag;  // [0] box check, [1] order check
     CK(ctx, flag.alloc(2));
@@ -662,6 +715,7 @@ pirk_status run_large(pirk_ctx* ctx, const pirk_model* m, int method, const pirk
     const auto t_setup = Clock::now();
     const uint64_t launches0 = ctx->launches;
     pirk_engine e;
+    e.cache_state = true;
     pirk_status st = engine_init(ctx, m, method, p, &e);
     if (st != PIRK_OK) return st;
     std::vector<uint64_t> slot_steps;
@@ -1053,6 +1107,7 @@ pirk_status pirk_create(int device, pirk_ctx** out) {
 void pirk_destroy(pirk_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
+    ctx->flush_cache();
     if (ctx->d_flags) cudaFree(ctx->d_flags);
     if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
