@@ -125,13 +125,26 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned b
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
+#ifndef PIRK_MBAR_HINT
+#define PIRK_MBAR_HINT 0  // try_wait suspend-time hint in ns (0: none)
+#endif
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+#if PIRK_MBAR_HINT > 0
+    // a waiting warp sleeps in try_wait instead of spinning on issue slots
+    asm volatile(
+        "{\n .reg .pred p;\nPIRK_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        " @!p bra PIRK_WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+        "r"(parity), "n"(PIRK_MBAR_HINT)
+        : "memory");
+#else
     asm volatile(
         "{\n .reg .pred p;\nPIRK_WAIT_%=:\n"
         " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
         " @!p bra PIRK_WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
         "r"(parity)
         : "memory");
+#endif
 }
 __device__ __forceinline__ void tma_load_plane(double* dst, const void* tmap, int x, int y, int z,
                                                unsigned long long* bar) {
