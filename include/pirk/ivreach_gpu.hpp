@@ -11,8 +11,10 @@
 //    vector fields are compiled device functors.  A model the device library
 //    does not implement throws std::invalid_argument("... no device kernel ...")
 //    -- there is no CPU fallback.
-//  * `workers` must be >= 1 (as in the reference); the call runs on the GPU of
-//    the thread's ivreach_gpu::Device (default cuda:0).
+//  * `workers` must be >= 1 (as in the reference); it selects the number of
+//    shard lanes (ivreach_gpu::Device::current(workers)): chain / heat3d runs
+//    shard the state across them and Monte Carlo the samples, bit-identical
+//    to workers = 1.
 // Exceptions and messages are the reference's: std::invalid_argument for
 // validation and missing capability, std::runtime_error for integration
 // failure, order violation and negative radius (reach.cpp:66-72, 107-117,
@@ -21,6 +23,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <new>
 #include <optional>
@@ -35,9 +38,11 @@ namespace ivreach_gpu {
 
 class Device {
 public:
-    explicit Device(int device = 0, pirk_mode mode = PIRK_MODE_EXACT) {
-        if (pirk_create(device, &ctx_) != PIRK_OK)
-            throw std::runtime_error("pirk_create: no usable CUDA device " + std::to_string(device));
+    explicit Device(int device = 0, pirk_mode mode = PIRK_MODE_EXACT) : Device(std::vector<int>{device}, mode) {}
+    // One shard lane per entry of `devices` (ids may repeat), see pirk_create_multi.
+    explicit Device(const std::vector<int>& devices, pirk_mode mode = PIRK_MODE_EXACT) {
+        if (pirk_create_multi(static_cast<int>(devices.size()), devices.data(), &ctx_) != PIRK_OK)
+            throw std::runtime_error("pirk_create: no usable CUDA device " + std::to_string(devices.at(0)));
         pirk_set_mode(ctx_, mode);
     }
     ~Device() { pirk_destroy(ctx_); }
@@ -45,13 +50,26 @@ public:
     Device& operator=(const Device&) = delete;
     pirk_ctx* get() const { return ctx_; }
     void set_mode(pirk_mode m) { pirk_set_mode(ctx_, m); }
+    int lanes() const { return pirk_lane_count(ctx_); }
 
-    // Process-wide default device.  Intentionally never destroyed: releasing
-    // CUDA resources from a static destructor can race the CUDA runtime's own
-    // teardown at exit.
-    static Device& current() {
-        static Device* dev = new Device(0);
-        return *dev;
+    // The context a reference call with `workers` runs on: `workers` shard
+    // lanes spread round-robin over the visible GPUs (workers == GPU count puts
+    // one shard on each GPU; on a one-GPU box the lanes share it).  One set of
+    // contexts per calling thread, so concurrent reference calls from distinct
+    // threads run on distinct contexts and streams.  Never
+    // destroyed: releasing CUDA resources from a static/thread-exit destructor
+    // can race the CUDA runtime's own teardown at exit.
+    static Device& current(int workers = 1) {
+        thread_local std::map<int, Device*> per_thread;
+        Device*& d = per_thread[workers];
+        if (!d) {
+            int count = pirk_device_count();
+            if (count < 1) count = 1;  // pirk_create_multi then reports the missing device
+            std::vector<int> devs(static_cast<std::size_t>(workers < 1 ? 1 : workers));
+            for (std::size_t r = 0; r < devs.size(); ++r) devs[r] = static_cast<int>(r % static_cast<std::size_t>(count));
+            d = new Device(devs);
+        }
+        return *d;
     }
 
 private:
@@ -229,7 +247,7 @@ ReachTube run(const ReachProblem& pr, int workers, const char* method, Call&& ca
     if (pr.initial.dim() != pr.model.dim)
         throw std::invalid_argument("problem: initial box dim " + std::to_string(pr.initial.dim()) +
                                     " does not match model dim " + std::to_string(pr.model.dim));
-    auto& dev = ivreach_gpu::Device::current();
+    auto& dev = ivreach_gpu::Device::current(workers);
     Marshal mar(pr);
     const std::size_t n = pr.model.dim;
     const std::uint64_t slots = pirk_record_schedule(pr.t0, pr.t1, pr.h, pr.tube_stride, nullptr, nullptr);

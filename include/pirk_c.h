@@ -29,8 +29,9 @@
  * CPU fallback anywhere behind this ABI.
  *
  * All host arrays are borrowed for the duration of a call.  Device pointers
- * (pirk_step_window) are caller-owned.  A pirk_ctx is not reentrant (like
- * Rk4Engine); distinct contexts may be used from distinct threads.
+ * (pirk_step_window) are caller-owned.  Calls on one pirk_ctx serialise on
+ * the context's mutex (like a non-reentrant Rk4Engine); distinct contexts run
+ * concurrently from distinct threads.
  */
 #ifndef PIRK_C_H
 #define PIRK_C_H
@@ -120,7 +121,7 @@ typedef struct pirk_report {
     uint64_t steps;
     uint64_t peak_state_bytes;   /* the reference's analytic value, for interface parity */
     uint64_t device_state_bytes; /* device bytes actually allocated for the state */
-    int32_t workers;             /* GPUs used (always 1 for a single context) */
+    int32_t workers;             /* shard lanes used (pirk_create_multi; 1 otherwise) */
     int32_t exact;               /* 1 = bit-exact arithmetic mode */
     double setup_s;
     double integration_s;
@@ -144,6 +145,21 @@ typedef struct pirk_engine pirk_engine;
 /* ---- context ---- */
 int32_t pirk_abi_version(void);
 pirk_status pirk_create(int device, pirk_ctx** out);
+/* A context of n_lanes shard lanes, lane r on CUDA device devices[r] (ids may
+ * repeat: several lanes then share one GPU).  Chain and heat3d MM/GB runs
+ * shard the state across the lanes (contiguous component ranges / z-slabs,
+ * 4-unit halos exchanged every RK4 step by peer copies over NVLink, boundary
+ * units first so the copies overlap the interior); Monte Carlo shards the
+ * sample range and min/max-folds the hulls.  Results are bit-identical for
+ * any lane count.  This is what the reference's `workers` argument maps to
+ * (reach.hpp:48,53,70).  Lane 0 is the primary device (pirk_set_stream). */
+pirk_status pirk_create_multi(int n_lanes, const int* devices, pirk_ctx** out);
+int32_t pirk_lane_count(const pirk_ctx* ctx);
+/* Visible CUDA devices (0 when there is none). */
+int32_t pirk_device_count(void);
+int32_t pirk_lane_device(const pirk_ctx* ctx, int32_t lane);
+/* Free the state buffers a context keeps between runs of the same size. */
+pirk_status pirk_release_cache(pirk_ctx* ctx);
 void pirk_destroy(pirk_ctx* ctx);
 const char* pirk_last_error(const pirk_ctx* ctx);
 pirk_status pirk_set_mode(pirk_ctx* ctx, int32_t mode);

@@ -158,6 +158,24 @@ def u01(seed, stream, index):
     return lib().po_u01(seed, stream, index)
 
 
+def _mix64(z):
+    """rng.hpp:11-16 on uint64 arrays (wrapping arithmetic)."""
+    z = z + np.uint64(0x9e3779b97f4a7c15)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xbf58476d1ce4e5b9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94d049bb133111eb)
+    return z ^ (z >> np.uint64(31))
+
+
+def u01_vec(seed, stream, index):
+    """rng.hpp:19-23 u01(seed, stream, index) vectorised over `index` (for
+    inputs of 1e7 components, where the per-call ctypes path is too slow)."""
+    with np.errstate(over="ignore"):
+        idx = np.asarray(index, dtype=np.uint64)
+        a = _mix64(np.uint64(seed)) ^ (np.uint64(stream) * np.uint64(0xd1342543de82ef95))
+        z = _mix64(_mix64(a) ^ (idx * np.uint64(0xaf251af3b0f025b5)))
+        return (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+
+
 def plan_steps(t0, t1, h):
     full = C.c_uint64()
     rem = C.c_int()
@@ -378,3 +396,53 @@ def ref_eval(model, which, x, p=None, xh=None, ph=None, t=0.0):
 
 def ref_max_threads():
     return ref_lib().ref_max_threads()
+
+
+# ------------------------------------------ uniform-box heat3d: the 1-D line
+
+def heat_line_uniform(g, value, steps, h, alpha=1.0, exchange=1.0, t0=0.0):
+    """heat3d (models.cpp:92-133) from a box that is uniform in every component,
+    in exact reference arithmetic, for ANY grid -- including C5's g = 1600.
+
+    Only the x = 0 face exchanges heat (Robin ghost, models.cpp:116-119); the
+    y and z faces are insulated (:121-125).  A field that is constant over
+    every (y, z) plane therefore stays so: each y/z stencil term is
+    ``x[i -+ g] - self == 0.0`` exactly, and ``acc + 0.0 == acc`` (up to the
+    sign of a zero, which == ignores).  Every component of the g^3 field
+    equals the 1-D line computed here with the reference's expression order:
+    acc = (x- term) + (x+ term), f = k*acc, and the RK4 update of rk4.cpp:38-68
+    (u = x + h2*k, x + h6*(((k0 + 2k1) + 2k2) + k3)), with the step plan of
+    rk4.cpp:8-17 / :99-100 for t1 = t0 + steps*h.  numpy's elementwise float64
+    add/mul are single IEEE operations (no contraction), so the result is
+    bit-exact.  Returns the line after `steps` steps (index = ix).
+    """
+    delta = 1.0 / float(g - 1)
+    k = alpha / (delta * delta)
+    robin = 2.0 * delta * exchange
+
+    def f(x):
+        acc = np.zeros_like(x)
+        acc[1:] = acc[1:] + (x[:-1] - x[1:])
+        acc[0] = acc[0] + ((x[1] - x[0]) - robin * x[0])
+        acc[:-1] = acc[:-1] + (x[1:] - x[:-1])
+        return k * acc
+
+    x = np.full(g, float(value))
+    plan = []
+    t1 = t0 + steps * h
+    span = t1 - t0
+    full = int(np.floor(span / h + 1e-9))
+    rem = span - float(full) * h
+    total = full + (1 if rem > 1e-9 * h else 0)
+    for kk in range(total):
+        t = t0 + float(kk) * h
+        plan.append((t1 - t) if kk + 1 == total else h)
+    for hk in plan:
+        h2 = 0.5 * hk
+        h6 = hk / 6.0
+        k0 = f(x)
+        k1 = f(x + h2 * k0)
+        k2 = f(x + h2 * k1)
+        k3 = f(x + hk * k2)
+        x = x + h6 * (((k0 + 2.0 * k1) + 2.0 * k2) + k3)
+    return x

@@ -12,7 +12,7 @@ from .models import (ARCH_QUAD, CHAIN, DECOMP_JACOBIAN, DECOMP_NATIVE, DECOMP_NO
                      with_jacobian_decomposition)
 from .reach import (Context, Engine, IntervalVector, MonteCarloSpec, PhaseTimes, ReachProblem,
                     ReachTube, RunReport, StepPlan, TubeEntry, center, contains, coverage_estimate,
-                    from_center_radius, get_context, growth_bound, half_width,
+                    from_center_radius, get_context, get_worker_context, growth_bound, half_width,
                     mixed_monotonicity, monte_carlo, monte_carlo_range, plan_steps,
                     record_schedule, sample_count, set_default_mode, step_window, subset_of,
                     tube_to_csv, validate)

@@ -106,6 +106,11 @@ _RP = C.POINTER(PirkReport)
 SIGNATURES = {
     "pirk_abi_version": (C.c_int32, []),
     "pirk_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "pirk_create_multi": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_void_p)]),
+    "pirk_lane_count": (C.c_int32, [C.c_void_p]),
+    "pirk_device_count": (C.c_int32, []),
+    "pirk_lane_device": (C.c_int32, [C.c_void_p, C.c_int32]),
+    "pirk_release_cache": (C.c_int, [C.c_void_p]),
     "pirk_destroy": (None, [C.c_void_p]),
     "pirk_last_error": (C.c_char_p, [C.c_void_p]),
     "pirk_set_mode": (C.c_int, [C.c_void_p, C.c_int32]),

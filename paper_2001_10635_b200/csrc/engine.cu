@@ -15,6 +15,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -26,10 +29,27 @@
 
 using namespace pirk;
 
+// A block of device memory kept for reuse by the next run of the same size.
+struct CachedBlock {
+    void* p;
+    size_t bytes;
+};
+
+// One shard lane of a multi-device context (pirk_create_multi): a device, its
+// compute and copy streams and its own state-buffer cache.  Lane 0 is the
+// context's primary device/stream (pirk_ctx::device / ::stream).
+struct PirkLane {
+    int device = 0;
+    cudaStream_t stream = nullptr;   // compute (owned)
+    cudaStream_t xstream = nullptr;  // halo sends (owned)
+    std::vector<CachedBlock> cache;
+};
+
 struct pirk_ctx {
     int device = 0;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t own_xstream = nullptr;  // lane 0's copy stream
     int mode = PIRK_MODE_EXACT;
     std::string err;
     uint64_t launches = 0;
@@ -37,14 +57,23 @@ struct pirk_ctx {
     unsigned long long* h_flags = nullptr;  // pinned mirror
     // state buffers of the last finished run, kept for the next run of the same
     // size: freeing 4 x 32 GB costs up to ~0.5 s of unmapping per call
-    struct Block {
-        void* p;
-        size_t bytes;
-    };
-    std::vector<Block> cache;
+    std::vector<CachedBlock> cache;
+    std::vector<PirkLane> peers;  // lanes 1 .. W-1 (empty for a one-device context)
+    // every ABI call on a context holds this: calls from several threads on one
+    // context serialise instead of racing on err / h_flags / the caches
+    std::recursive_mutex mu;
+    int lanes() const { return 1 + static_cast<int>(peers.size()); }
     void flush_cache() {
-        for (const Block& b : cache) cudaFree(b.p);
+        for (const CachedBlock& b : cache) cudaFree(b.p);
         cache.clear();
+    }
+    // every lane's cache (device allocations retry after this on OOM)
+    void flush_all() {
+        flush_cache();
+        for (PirkLane& l : peers) {
+            for (const CachedBlock& b : l.cache) cudaFree(b.p);
+            l.cache.clear();
+        }
     }
 };
 
@@ -63,6 +92,8 @@ pirk_status cuda_fail(pirk_ctx* ctx, cudaError_t e, const char* what) {
     if (e == cudaErrorMemoryAllocation) cudaGetLastError();  // clear the sticky-free error
     return fail(ctx, st, std::string(what) + ": " + cudaGetErrorString(e));
 }
+
+#define LOCK(ctx) std::lock_guard<std::recursive_mutex> lock_guard_((ctx)->mu)
 
 #define CK(ctx, expr)                                                  \
     do {                                                               \
@@ -340,35 +371,57 @@ bool check_problem(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p, bo
     return true;
 }
 
+// cudaMalloc that, on out-of-memory, releases every cached state block of the
+// context and tries once more (the cache must never cause an OOM).
+cudaError_t dev_malloc(pirk_ctx* ctx, void** p, size_t bytes) {
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaErrorMemoryAllocation && ctx) {
+        cudaGetLastError();
+        ctx->flush_all();
+        e = cudaMalloc(p, bytes);
+    }
+    return e;
+}
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
-    pirk_ctx* owner = nullptr;  // set: a state buffer that returns to owner->cache
+    std::vector<CachedBlock>* cache = nullptr;  // set: a state buffer that returns to this cache
     size_t bytes = 0;
-    ~DevBuf() {
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
         if (!p) return;
-        if (owner && owner->cache.size() < 8) {
-            owner->cache.push_back({p, bytes});
+        if (cache && cache->size() < 8) {
+            cache->push_back({p, bytes});
         } else {
             cudaFree(p);
         }
+        p = nullptr;
     }
-    cudaError_t alloc(size_t count) { return cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T) + 16); }
-    // take a cached block of exactly this size, else drop the cache (it was sized
-    // for another problem) and allocate
-    cudaError_t alloc_state(pirk_ctx* ctx, size_t count) {
+    cudaError_t alloc(pirk_ctx* ctx, size_t count) {
         bytes = count * sizeof(T) + 16;
-        owner = ctx;
-        for (size_t i = 0; i < ctx->cache.size(); ++i) {
-            if (ctx->cache[i].bytes == bytes) {
-                p = static_cast<T*>(ctx->cache[i].p);
-                ctx->cache.erase(ctx->cache.begin() + static_cast<long>(i));
+        return dev_malloc(ctx, reinterpret_cast<void**>(&p), bytes);
+    }
+    // take a cached block of exactly this size from `c`, else drop `c` (it was
+    // sized for another problem) and allocate
+    cudaError_t alloc_state(pirk_ctx* ctx, std::vector<CachedBlock>& c, size_t count) {
+        bytes = count * sizeof(T) + 16;
+        cache = &c;
+        for (size_t i = 0; i < c.size(); ++i) {
+            if (c[i].bytes == bytes) {
+                p = static_cast<T*>(c[i].p);
+                c.erase(c.begin() + static_cast<long>(i));
                 return cudaSuccess;
             }
         }
-        ctx->flush_cache();
-        return cudaMalloc(reinterpret_cast<void**>(&p), bytes);
+        for (const CachedBlock& b : c) cudaFree(b.p);
+        c.clear();
+        return dev_malloc(ctx, reinterpret_cast<void**>(&p), bytes);
     }
+    cudaError_t alloc_state(pirk_ctx* ctx, size_t count) { return alloc_state(ctx, ctx->cache, count); }
 };
 
 bool exact_mode(const pirk_ctx* ctx) { return ctx->mode == PIRK_MODE_EXACT; }
@@ -382,17 +435,16 @@ bool state_cache_on() {
     return on;
 }
 
-cudaError_t step_launch(pirk_ctx* ctx, const pirk_model* m, int method, const ChainModel& cm,
+cudaError_t step_launch(pirk_ctx* ctx, cudaStream_t stream, const pirk_model* m, const ChainModel& cm,
                         const HeatModel& hm, const WindowArgs& w, const StepConsts& sc,
                         uint64_t k, unsigned long long* fail_ptr) {
     ctx->launches++;
     const bool ex = exact_mode(ctx);
-    (void)method;
     if (is_chain(m))
-        return ex ? launch_chain_step<true>(cm, w, sc, k, fail_ptr, ctx->stream)
-                  : launch_chain_step<false>(cm, w, sc, k, fail_ptr, ctx->stream);
-    return ex ? launch_heat_step<true>(hm, w, sc, k, fail_ptr, ctx->stream)
-              : launch_heat_step<false>(hm, w, sc, k, fail_ptr, ctx->stream);
+        return ex ? launch_chain_step<true>(cm, w, sc, k, fail_ptr, stream)
+                  : launch_chain_step<false>(cm, w, sc, k, fail_ptr, stream);
+    return ex ? launch_heat_step<true>(hm, w, sc, k, fail_ptr, stream)
+              : launch_heat_step<false>(hm, w, sc, k, fail_ptr, stream);
 }
 
 std::string integ_msg(uint64_t step, uint64_t comp, double t) {
@@ -478,12 +530,12 @@ pirk_status engine_init(pirk_ctx* ctx, const pirk_model* m, int method, const pi
         CK(ctx, e->b0.alloc_state(ctx, n));
         CK(ctx, e->b1.alloc_state(ctx, n));
     } else {
-        CK(ctx, e->a0.alloc(n));
-        CK(ctx, e->a1.alloc(n));
-        CK(ctx, e->b0.alloc(n));
-        CK(ctx, e->b1.alloc(n));
+        CK(ctx, e->a0.alloc(ctx, n));
+        CK(ctx, e->a1.alloc(ctx, n));
+        CK(ctx, e->b0.alloc(ctx, n));
+        CK(ctx, e->b1.alloc(ctx, n));
     }
-    CK(ctx, e->d_fail.alloc(2));
+    CK(ctx, e->d_fail.alloc(ctx, 2));
     CK(ctx, cudaMemsetAsync(e->d_fail.p, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
     CK(ctx, cudaMemcpyAsync(e->a0.p, p->init_lower, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CK(ctx, cudaMemcpyAsync(e->a1.p, p->init_upper, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
@@ -550,7 +602,7 @@ pirk_status engine_advance(pirk_engine* e, uint64_t nsteps) {
         const uint64_t k = e->done;
         const StepConsts sc = host_step(e->t0, e->t1, e->h, k, e->plan.total);
         WindowArgs w{e->s0(), e->s1(), e->o0(), e->o1(), 0, e->units, 0, e->units};
-        CK(ctx, step_launch(ctx, &e->model, e->method, e->cm, e->hm, w, sc, k, e->d_fail.p));
+        CK(ctx, step_launch(ctx, ctx->stream, &e->model, e->cm, e->hm, w, sc, k, e->d_fail.p));
         e->cur ^= 1;
         e->done++;
     }
@@ -609,13 +661,13 @@ pirk_status run_heat_mm_pipelined(pirk_ctx* ctx, const pirk_model* m, const pirk
     e.hm = heat_model(m, PIRK_METHOD_MM);
     const size_t n = e.n;
     const bool cache = state_cache_on();
-    CK(ctx, cache ? e.a0.alloc_state(ctx, n) : e.a0.alloc(n));
-    CK(ctx, cache ? e.a1.alloc_state(ctx, n) : e.a1.alloc(n));
-    CK(ctx, cache ? e.b0.alloc_state(ctx, n) : e.b0.alloc(n));
-    CK(ctx, cache ? e.b1.alloc_state(ctx, n) : e.b1.alloc(n));
-    CK(ctx, e.d_fail.alloc(2));
+    CK(ctx, cache ? e.a0.alloc_state(ctx, n) : e.a0.alloc(ctx, n));
+    CK(ctx, cache ? e.a1.alloc_state(ctx, n) : e.a1.alloc(ctx, n));
+    CK(ctx, cache ? e.b0.alloc_state(ctx, n) : e.b0.alloc(ctx, n));
+    CK(ctx, cache ? e.b1.alloc_state(ctx, n) : e.b1.alloc(ctx, n));
+    CK(ctx, e.d_fail.alloc(ctx, 2));
     DevBuf<unsigned long long> flag;  // [0] box check, [1] order check
-    CK(ctx, flag.alloc(2));
+    CK(ctx, flag.alloc(ctx, 2));
     StreamGuard xs;
     CK(ctx, cudaStreamCreateWithFlags(&xs.s, cudaStreamNonBlocking));
     EventGuard ev_h0, ev_h1, ev_c0, ev_x;
@@ -694,6 +746,65 @@ pirk_status run_heat_mm_pipelined(pirk_ctx* ctx, const pirk_model* m, const pirk
     return PIRK_OK;
 }
 
+// The error contract of a finished large-model run, in the reference's order
+// of detection (reach.cpp:107-117, 121-134, 181-192), and the report.  f0/f1:
+// the minimum failure keys of the two fields; flags/vals: per recorded slot
+// the minimum violating component (order / negative radius) and its radius.
+pirk_status large_errors(pirk_ctx* ctx, int method, const pirk_problem* p, uint64_t total,
+                         const std::vector<uint64_t>& slot_steps, const std::vector<double>& slot_times,
+                         unsigned long long f0, unsigned long long f1,
+                         const std::vector<unsigned long long>& flags, const std::vector<double>& vals,
+                         uint64_t n, uint64_t dev_bytes, double setup_s, double integ_s,
+                         uint64_t launches, int workers, pirk_report* rep) {
+    const uint64_t S = slot_steps.size();
+    auto decode = [](unsigned long long key, uint64_t& step, uint64_t& comp) {
+        step = key >> kFailCompBits;
+        comp = key & ((1ull << kFailCompBits) - 1);
+    };
+    if (method == PIRK_METHOD_MM) {
+        uint64_t fs = 0, fc = 0;
+        if (f0 != kNoFail) decode(f0, fs, fc);
+        for (uint64_t s = 0; s < S; ++s) {
+            // an integration failure in step k is raised before slot k+1 is observed
+            if (f0 != kNoFail && fs < slot_steps[s])
+                return fail(ctx, PIRK_EINTEGRATION, "mixed-monotonicity embedding integration: " +
+                                                        integ_msg(fs, fc, p->t0 + static_cast<double>(fs) * p->h));
+            if (flags[s] != kNoFail)
+                return fail(ctx, PIRK_EORDER, "mixed-monotonicity: embedding order violated at step " +
+                                                  std::to_string(slot_steps[s]) + ", t = " + fstr(slot_times[s]) +
+                                                  ", component " + std::to_string(flags[s]));
+        }
+        if (f0 != kNoFail)
+            return fail(ctx, PIRK_EINTEGRATION, "mixed-monotonicity embedding integration: " +
+                                                    integ_msg(fs, fc, p->t0 + static_cast<double>(fs) * p->h));
+        fill_report(rep, n, 0, total, 7 * 2 * n * sizeof(double), dev_bytes, exact_mode(ctx), setup_s,
+                    integ_s, 0.0, launches);
+    } else {
+        // center integration runs to completion before the radius integration
+        // (reach.cpp:103-117), and the clamp pass follows both (reach.cpp:121-134)
+        uint64_t fs = 0, fc = 0;
+        if (f0 != kNoFail) {
+            decode(f0, fs, fc);
+            return fail(ctx, PIRK_EINTEGRATION, "growth-bound center integration: " +
+                                                    integ_msg(fs, fc, p->t0 + static_cast<double>(fs) * p->h));
+        }
+        if (f1 != kNoFail) {
+            decode(f1, fs, fc);
+            return fail(ctx, PIRK_EINTEGRATION, "growth-bound radius integration: " +
+                                                    integ_msg(fs, fc, p->t0 + static_cast<double>(fs) * p->h));
+        }
+        for (uint64_t s = 0; s < S; ++s)
+            if (flags[s] != kNoFail)
+                return fail(ctx, PIRK_ENEGRADIUS, "growth-bound: deviation went negative (" + fstr(vals[s]) +
+                                                      ") at component " + std::to_string(flags[s]) +
+                                                      "; contraction matrix is invalid");
+        fill_report(rep, n, 0, total, 7 * n * sizeof(double), dev_bytes, exact_mode(ctx), setup_s, integ_s,
+                    0.0, launches);
+    }
+    if (rep) rep->workers = workers;
+    return PIRK_OK;
+}
+
 // Large-model (chain / heat kernels) MM and GB driver.
 pirk_status run_large(pirk_ctx* ctx, const pirk_model* m, int method, const pirk_problem* p,
                       pirk_tube* tube, pirk_report* rep) {
@@ -727,8 +838,8 @@ pirk_status run_large(pirk_ctx* ctx, const pirk_model* m, int method, const pirk
                                           " < record slots " + std::to_string(S));
     DevBuf<unsigned long long> slot_flag;  // per slot: order (MM) / negative radius (GB)
     DevBuf<double> slot_val;
-    CK(ctx, slot_flag.alloc(S));
-    CK(ctx, slot_val.alloc(S));
+    CK(ctx, slot_flag.alloc(ctx, S));
+    CK(ctx, slot_val.alloc(ctx, S));
     CK(ctx, cudaMemsetAsync(slot_flag.p, 0xff, S * sizeof(unsigned long long), ctx->stream));
     CK(ctx, cudaStreamSynchronize(ctx->stream));
     const double setup_s = since(t_setup);
@@ -769,53 +880,250 @@ pirk_status run_large(pirk_ctx* ctx, const pirk_model* m, int method, const pirk
         if (tube->times)
             for (uint64_t s = 0; s < S; ++s) tube->times[s] = slot_times[s];
     }
-    // ---- error contract, in the reference's order of detection
-    const unsigned long long f0 = ctx->h_flags[0], f1 = ctx->h_flags[1];
-    auto decode = [](unsigned long long key, uint64_t& step, uint64_t& comp) {
-        step = key >> kFailCompBits;
-        comp = key & ((1ull << kFailCompBits) - 1);
-    };
-    if (method == PIRK_METHOD_MM) {
-        uint64_t fs = 0, fc = 0;
-        if (f0 != kNoFail) decode(f0, fs, fc);
-        for (uint64_t s = 0; s < S; ++s) {
-            // an integration failure in step k is raised before slot k+1 is observed
-            if (f0 != kNoFail && fs < slot_steps[s])
-                return fail(ctx, PIRK_EINTEGRATION, "mixed-monotonicity embedding integration: " +
-                                                        integ_msg(fs, fc, p->t0 + static_cast<double>(fs) * p->h));
-            if (flags[s] != kNoFail)
-                return fail(ctx, PIRK_EORDER, "mixed-monotonicity: embedding order violated at step " +
-                                                  std::to_string(slot_steps[s]) + ", t = " + fstr(slot_times[s]) +
-                                                  ", component " + std::to_string(flags[s]));
-        }
-        if (f0 != kNoFail)
-            return fail(ctx, PIRK_EINTEGRATION, "mixed-monotonicity embedding integration: " +
-                                                    integ_msg(fs, fc, p->t0 + static_cast<double>(fs) * p->h));
-        fill_report(rep, n, 0, e.plan.total, 7 * 2 * n * sizeof(double), 4 * n * sizeof(double),
-                    exact_mode(ctx), setup_s, integ_s, 0.0, ctx->launches - launches0);
-    } else {
-        // center integration runs to completion before the radius integration
-        // (reach.cpp:103-117), and the clamp pass follows both (reach.cpp:121-134)
-        uint64_t fs = 0, fc = 0;
-        if (f0 != kNoFail) {
-            decode(f0, fs, fc);
-            return fail(ctx, PIRK_EINTEGRATION, "growth-bound center integration: " +
-                                                    integ_msg(fs, fc, p->t0 + static_cast<double>(fs) * p->h));
-        }
-        if (f1 != kNoFail) {
-            decode(f1, fs, fc);
-            return fail(ctx, PIRK_EINTEGRATION, "growth-bound radius integration: " +
-                                                    integ_msg(fs, fc, p->t0 + static_cast<double>(fs) * p->h));
-        }
-        for (uint64_t s = 0; s < S; ++s)
-            if (flags[s] != kNoFail)
-                return fail(ctx, PIRK_ENEGRADIUS, "growth-bound: deviation went negative (" + fstr(vals[s]) +
-                                                      ") at component " + std::to_string(flags[s]) +
-                                                      "; contraction matrix is invalid");
-        fill_report(rep, n, 0, e.plan.total, 7 * n * sizeof(double), 4 * n * sizeof(double),
-                    exact_mode(ctx), setup_s, integ_s, 0.0, ctx->launches - launches0);
+    return large_errors(ctx, method, p, e.plan.total, slot_steps, slot_times, ctx->h_flags[0],
+                        ctx->h_flags[1], flags, vals, n, 4 * n * sizeof(double), setup_s, integ_s,
+                        ctx->launches - launches0, 1, rep);
+}
+
+// ------------------------------------------------ multi-lane (state-sharded) driver
+//
+// A context made by pirk_create_multi owns W lanes (device + compute stream +
+// copy stream).  Chains shard contiguous component ranges, heat3d contiguous
+// z-slabs (models.cpp:110-112), exactly as sharded.py does across processes.
+// Each lane keeps a window of its units plus a 4-unit halo per side (the RK4
+// dependency cone of a radius-1 stencil) and exchanges halos every step by
+// copy-engine peer copies over NVLink:
+//
+//   lane stream:  wait(halos of step k-1) | boundary units | interior units ....
+//   lane copies:                          | send boundary -> neighbours' halos
+//
+// The boundary units (the ones the neighbours need next step) are computed
+// first, their peer copies run while the interior computes, and the next
+// step waits only for the copies (double-buffered events: a lane waits on
+// its neighbours' step-(k-1) records, never on the current ones).  Every unit
+// is computed once from the same inputs as on one device, so the result is
+// bit-identical for any lane count, and lanes on the SAME device (a repeated
+// device id) run the identical code path with device-local copies -- which is
+// how the path is tested on a one-GPU box.
+struct LaneRef {
+    int device;
+    cudaStream_t s, xs;
+    std::vector<CachedBlock>* cache;
+};
+
+LaneRef lane_ref(pirk_ctx* ctx, int r) {
+    if (r == 0) return {ctx->device, ctx->stream, ctx->own_xstream, &ctx->cache};
+    PirkLane& l = ctx->peers[static_cast<size_t>(r - 1)];
+    return {l.device, l.stream, l.xstream, &l.cache};
+}
+
+struct ShardState {
+    LaneRef L{};
+    uint64_t b = 0, e = 0, wb = 0, we = 0;  // owned units [b, e), window [wb, we)
+    DevBuf<double> a0, a1, b0, b1;
+    DevBuf<unsigned long long> fail, slot_flag, box_flag;
+    DevBuf<double> slot_val;
+    int cur = 0;
+    cudaEvent_t bnd = nullptr, sent[2] = {nullptr, nullptr};
+    double* in0() { return cur ? b0.p : a0.p; }
+    double* in1() { return cur ? b1.p : a1.p; }
+    double* out0() { return cur ? a0.p : b0.p; }
+    double* out1() { return cur ? a1.p : b1.p; }
+    ~ShardState() {
+        for (cudaEvent_t ev : {bnd, sent[0], sent[1]})
+            if (ev) cudaEventDestroy(ev);
     }
-    return PIRK_OK;
+};
+
+// lanes a run of `units` partition units can use: >= 8 units per lane, so a
+// 4-unit halo always comes from the adjacent lane alone
+int usable_lanes(const pirk_ctx* ctx, uint64_t units) {
+    const uint64_t w = std::min<uint64_t>(static_cast<uint64_t>(ctx->lanes()), units / 8);
+    return w < 1 ? 1 : static_cast<int>(w);
+}
+
+pirk_status run_large_multi(pirk_ctx* ctx, const pirk_model* m, int method, const pirk_problem* p,
+                            pirk_tube* tube, pirk_report* rep) {
+    const auto t_setup = Clock::now();
+    const uint64_t launches0 = ctx->launches;
+    Plan plan;
+    plan_steps(p->t0, p->t1, p->h, plan);
+    if (plan.total >= (1ull << 23))
+        return fail(ctx, PIRK_EINVAL, "step count exceeds the device failure-key range (2^23)");
+    const uint64_t n = m->dim;
+    const uint64_t unit = is_heat(m) ? m->grid * m->grid : 1;
+    const uint64_t units = n / unit;
+    if (2 * n >= (1ull << kFailCompBits))
+        return fail(ctx, PIRK_EINVAL, "dimension exceeds the device failure-key range");
+    const int W = usable_lanes(ctx, units);
+    std::vector<uint64_t> slot_steps;
+    std::vector<double> slot_times;
+    record_schedule(p->t0, p->t1, p->h, p->tube_stride, plan, slot_steps, slot_times);
+    const uint64_t S = slot_steps.size();
+    if (tube && tube->max_slots < S)
+        return fail(ctx, PIRK_EINVAL, "tube: max_slots " + std::to_string(tube->max_slots) +
+                                          " < record slots " + std::to_string(S));
+    double p0 = 0.0, p1 = 0.0;
+    if (m->input_dim > 0) {
+        if (method == PIRK_METHOD_MM) {
+            p0 = p->input_lower[0];
+            p1 = p->input_upper[0];
+        } else {  // interval.cpp:25-37 center / half-width
+            p0 = 0.5 * (p->input_upper[0] + p->input_lower[0]);
+            p1 = 0.5 * (p->input_upper[0] - p->input_lower[0]);
+        }
+    }
+    const ChainModel cm = chain_model(m, method, p0, p1);
+    const HeatModel hm = heat_model(m, method);
+    const bool cache = state_cache_on();
+    std::unique_ptr<ShardState[]> sh(new ShardState[static_cast<size_t>(W)]);
+    uint64_t dev_bytes = 0;
+    for (int r = 0; r < W; ++r) {
+        ShardState& z = sh[static_cast<size_t>(r)];
+        z.L = lane_ref(ctx, r);
+        z.b = units * static_cast<uint64_t>(r) / static_cast<uint64_t>(W);
+        z.e = units * static_cast<uint64_t>(r + 1) / static_cast<uint64_t>(W);
+        z.wb = z.b >= 4 ? z.b - 4 : 0;
+        z.we = std::min(z.e + 4, units);
+        const size_t wn = (z.we - z.wb) * unit;
+        CK(ctx, cudaSetDevice(z.L.device));
+        for (DevBuf<double>* d : {&z.a0, &z.a1, &z.b0, &z.b1})
+            CK(ctx, cache ? d->alloc_state(ctx, *z.L.cache, wn) : d->alloc(ctx, wn));
+        dev_bytes += 4 * wn * sizeof(double);
+        CK(ctx, z.fail.alloc(ctx, 2));
+        CK(ctx, z.slot_flag.alloc(ctx, S));
+        CK(ctx, z.slot_val.alloc(ctx, S));
+        CK(ctx, z.box_flag.alloc(ctx, 1));
+        for (cudaEvent_t* ev : {&z.bnd, &z.sent[0], &z.sent[1]})
+            CK(ctx, cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+        CK(ctx, cudaMemsetAsync(z.fail.p, 0xff, 2 * sizeof(unsigned long long), z.L.s));
+        CK(ctx, cudaMemsetAsync(z.slot_flag.p, 0xff, S * sizeof(unsigned long long), z.L.s));
+        CK(ctx, cudaMemsetAsync(z.box_flag.p, 0xff, sizeof(unsigned long long), z.L.s));
+        CK(ctx, cudaMemcpyAsync(z.a0.p, p->init_lower + z.wb * unit, wn * sizeof(double), cudaMemcpyHostToDevice, z.L.s));
+        CK(ctx, cudaMemcpyAsync(z.a1.p, p->init_upper + z.wb * unit, wn * sizeof(double), cudaMemcpyHostToDevice, z.L.s));
+        const size_t own = (z.b - z.wb) * unit;
+        CK(ctx, launch_box_check(z.a0.p + own, z.a1.p + own, (z.e - z.b) * unit, z.box_flag.p, z.L.s));
+        ctx->launches++;
+        if (method == PIRK_METHOD_GB) {
+            CK(ctx, launch_center_radius(z.a0.p, z.a1.p, wn, z.L.s));
+            ctx->launches++;
+        }
+    }
+    const double setup_s = since(t_setup);
+    const auto t_int = Clock::now();
+    const bool ex = exact_mode(ctx);
+    auto launch = [&](ShardState& z, const StepConsts& sc, uint64_t k, uint64_t ob, uint64_t oe) -> cudaError_t {
+        if (ob >= oe) return cudaSuccess;
+        const size_t off = (ob - z.wb) * unit;
+        WindowArgs w{z.in0(), z.in1(), z.out0() + off, z.out1() + off, z.wb, z.we, ob, oe};
+        ctx->launches++;
+        if (is_chain(m))
+            return ex ? launch_chain_step<true>(cm, w, sc, k, z.fail.p, z.L.s)
+                      : launch_chain_step<false>(cm, w, sc, k, z.fail.p, z.L.s);
+        return ex ? launch_heat_step<true>(hm, w, sc, k, z.fail.p, z.L.s)
+                  : launch_heat_step<false>(hm, w, sc, k, z.fail.p, z.L.s);
+    };
+    const size_t halo_bytes = 4 * unit * sizeof(double);
+    uint64_t done = 0;
+    for (uint64_t s = 0; s < S; ++s) {
+        for (; done < slot_steps[s]; ++done) {
+            const uint64_t k = done;
+            const StepConsts sc = host_step(p->t0, p->t1, p->h, k, plan.total);
+            for (int r = 0; r < W; ++r) {
+                ShardState& z = sh[static_cast<size_t>(r)];
+                const bool left = r > 0, right = r + 1 < W;
+                CK(ctx, cudaSetDevice(z.L.device));
+                if (k > 0) {  // this step's inputs include the halos the neighbours sent last step
+                    if (left) CK(ctx, cudaStreamWaitEvent(z.L.s, sh[static_cast<size_t>(r - 1)].sent[(k - 1) & 1], 0));
+                    if (right) CK(ctx, cudaStreamWaitEvent(z.L.s, sh[static_cast<size_t>(r + 1)].sent[(k - 1) & 1], 0));
+                }
+                // 1. boundary units, the ones the neighbours read next step
+                if (left) CK(ctx, launch(z, sc, k, z.b, z.b + 4));
+                if (right) CK(ctx, launch(z, sc, k, z.e - 4, z.e));
+                // 2. their peer copies, on the copy stream
+                if (left || right) {
+                    CK(ctx, cudaEventRecord(z.bnd, z.L.s));
+                    CK(ctx, cudaStreamWaitEvent(z.L.xs, z.bnd, 0));
+                    if (left) {
+                        ShardState& y = sh[static_cast<size_t>(r - 1)];
+                        const size_t so = (z.b - z.wb) * unit, dof = (z.b - y.wb) * unit;
+                        CK(ctx, cudaMemcpyPeerAsync(y.out0() + dof, y.L.device, z.out0() + so, z.L.device, halo_bytes, z.L.xs));
+                        CK(ctx, cudaMemcpyPeerAsync(y.out1() + dof, y.L.device, z.out1() + so, z.L.device, halo_bytes, z.L.xs));
+                    }
+                    if (right) {
+                        ShardState& y = sh[static_cast<size_t>(r + 1)];
+                        const size_t so = (z.e - 4 - z.wb) * unit, dof = (z.e - 4 - y.wb) * unit;
+                        CK(ctx, cudaMemcpyPeerAsync(y.out0() + dof, y.L.device, z.out0() + so, z.L.device, halo_bytes, z.L.xs));
+                        CK(ctx, cudaMemcpyPeerAsync(y.out1() + dof, y.L.device, z.out1() + so, z.L.device, halo_bytes, z.L.xs));
+                    }
+                    CK(ctx, cudaEventRecord(z.sent[k & 1], z.L.xs));
+                }
+                // 3. the interior, overlapping the copies
+                CK(ctx, launch(z, sc, k, left ? z.b + 4 : z.b, right ? z.e - 4 : z.e));
+            }
+            for (int r = 0; r < W; ++r) sh[static_cast<size_t>(r)].cur ^= 1;
+        }
+        for (int r = 0; r < W; ++r) {  // record slot s on every lane's owned units
+            ShardState& z = sh[static_cast<size_t>(r)];
+            CK(ctx, cudaSetDevice(z.L.device));
+            const size_t own = (z.b - z.wb) * unit, cnt = (z.e - z.b) * unit;
+            const double* lo = z.in0() + own;
+            const double* hi = z.in1() + own;
+            if (method == PIRK_METHOD_MM) {
+                CK(ctx, launch_order_check(lo, hi, cnt, z.slot_flag.p + s, z.L.s));
+            } else {  // the next step's output buffers (owned part) take the clamped box
+                CK(ctx, launch_gb_box(lo, hi, z.out0() + own, z.out1() + own, cnt, z.slot_flag.p + s, z.L.s));
+                CK(ctx, launch_gb_negval(hi, z.slot_flag.p + s, z.slot_val.p + s, z.L.s));
+                ctx->launches++;
+                lo = z.out0() + own;
+                hi = z.out1() + own;
+            }
+            ctx->launches++;
+            if (tube && tube->lower)
+                CK(ctx, cudaMemcpyAsync(tube->lower + s * n + z.b * unit, lo, cnt * sizeof(double), cudaMemcpyDeviceToHost, z.L.s));
+            if (tube && tube->upper)
+                CK(ctx, cudaMemcpyAsync(tube->upper + s * n + z.b * unit, hi, cnt * sizeof(double), cudaMemcpyDeviceToHost, z.L.s));
+        }
+    }
+    unsigned long long f0 = kNoFail, f1 = kNoFail, box = kNoFail;
+    std::vector<unsigned long long> flags(S, kNoFail), lf(S);
+    std::vector<double> vals(S, 0.0), lv(S);
+    for (int r = 0; r < W; ++r) {
+        ShardState& z = sh[static_cast<size_t>(r)];
+        CK(ctx, cudaSetDevice(z.L.device));
+        unsigned long long hf[3];
+        CK(ctx, cudaMemcpyAsync(hf, z.fail.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, z.L.s));
+        CK(ctx, cudaMemcpyAsync(hf + 2, z.box_flag.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, z.L.s));
+        CK(ctx, cudaMemcpyAsync(lf.data(), z.slot_flag.p, S * sizeof(unsigned long long), cudaMemcpyDeviceToHost, z.L.s));
+        CK(ctx, cudaMemcpyAsync(lv.data(), z.slot_val.p, S * sizeof(double), cudaMemcpyDeviceToHost, z.L.s));
+        CK(ctx, cudaStreamSynchronize(z.L.s));
+        CK(ctx, cudaStreamSynchronize(z.L.xs));
+        // failure keys carry global components; slot / box flags are lane-local
+        f0 = std::min(f0, hf[0]);
+        f1 = std::min(f1, hf[1]);
+        const unsigned long long base = z.b * unit;
+        if (hf[2] != kNoFail) box = std::min(box, hf[2] + base);
+        for (uint64_t s = 0; s < S; ++s)
+            if (lf[s] != kNoFail && lf[s] + base < flags[s]) {
+                flags[s] = lf[s] + base;
+                vals[s] = lv[s];
+            }
+    }
+    CK(ctx, cudaSetDevice(ctx->device));
+    const double integ_s = since(t_int);
+    if (box != kNoFail) {  // IntervalVector validation (interval.cpp:14-22) comes first
+        const bool nonfinite = !std::isfinite(p->init_lower[box]) || !std::isfinite(p->init_upper[box]);
+        return fail(ctx, PIRK_EINVAL, std::string(nonfinite ? "interval: non-finite bound at component "
+                                                            : "interval: lower > upper at component ") +
+                                          std::to_string(box));
+    }
+    if (tube) {
+        tube->n_slots = S;
+        if (tube->times)
+            for (uint64_t s = 0; s < S; ++s) tube->times[s] = slot_times[s];
+    }
+    return large_errors(ctx, method, p, plan.total, slot_steps, slot_times, f0, f1, flags, vals, n, dev_bytes,
+                        setup_s, integ_s, ctx->launches - launches0, W, rep);
 }
 
 // Small-model MM / GB: one device thread per integration.
@@ -845,10 +1153,10 @@ pirk_status run_small(pirk_ctx* ctx, const pirk_model* m, int method, const pirk
         for (uint64_t j = 0; j < ni; ++j) { pp[j] = p->input_lower[j]; pp[ni + j] = p->input_upper[j]; }
         DevBuf<double> dx, dp, drec;
         DevBuf<unsigned long long> dfail;
-        CK(ctx, dx.alloc(2 * n));
-        CK(ctx, dp.alloc(pp.size()));
-        CK(ctx, drec.alloc(S * 2 * n));
-        CK(ctx, dfail.alloc(1));
+        CK(ctx, dx.alloc(ctx, 2 * n));
+        CK(ctx, dp.alloc(ctx, pp.size()));
+        CK(ctx, drec.alloc(ctx, S * 2 * n));
+        CK(ctx, dfail.alloc(ctx, 1));
         CK(ctx, cudaMemcpyAsync(dx.p, x0.data(), 2 * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
         CK(ctx, cudaMemcpyAsync(dp.p, pp.data(), pp.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
         CK(ctx, cudaMemsetAsync(dfail.p, 0xff, sizeof(unsigned long long), ctx->stream));
@@ -873,8 +1181,8 @@ pirk_status run_small(pirk_ctx* ctx, const pirk_model* m, int method, const pirk
         }
         DevBuf<double> dc, dr, dpc, dw, drec0, drec1;
         DevBuf<unsigned long long> dfail;
-        CK(ctx, dc.alloc(n)); CK(ctx, dr.alloc(n)); CK(ctx, dpc.alloc(ni + 1)); CK(ctx, dw.alloc(ni + 1));
-        CK(ctx, drec0.alloc(S * n)); CK(ctx, drec1.alloc(S * n)); CK(ctx, dfail.alloc(2));
+        CK(ctx, dc.alloc(ctx, n)); CK(ctx, dr.alloc(ctx, n)); CK(ctx, dpc.alloc(ctx, ni + 1)); CK(ctx, dw.alloc(ctx, ni + 1));
+        CK(ctx, drec0.alloc(ctx, S * n)); CK(ctx, drec1.alloc(ctx, S * n)); CK(ctx, dfail.alloc(ctx, 2));
         CK(ctx, cudaMemcpyAsync(dc.p, c0.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
         CK(ctx, cudaMemcpyAsync(dr.p, r0.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
         CK(ctx, cudaMemcpyAsync(dpc.p, pc.data(), (ni + 1) * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
@@ -961,6 +1269,11 @@ pirk_status run_small(pirk_ctx* ctx, const pirk_model* m, int method, const pirk
     return PIRK_OK;
 }
 
+// Monte Carlo (reach.cpp:246-323): samples [s_begin, s_end) split over the
+// context's lanes (pirk_create_multi), each lane one launch of the
+// one-sample-per-thread kernel on its own device/stream; the per-lane hulls
+// (order-preserving keys) are min/max-folded on the host -- exact and
+// order-independent, the single-process form of the NCCL MIN/MAX all-reduce.
 pirk_status run_mc(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p, uint64_t seed,
                    uint64_t s_begin, uint64_t s_end, uint64_t m_total, pirk_tube* tube,
                    bool fold_into, pirk_report* rep, const double* box_lo, const double* box_hi,
@@ -982,8 +1295,6 @@ pirk_status run_mc(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p, ui
         return fail(ctx, PIRK_EINVAL, "monte_carlo: sample count or step count exceeds the device key range");
     const uint64_t n = m->dim, ni = m->input_dim;
     const SmallModel sm = small_model(m);
-    DevBuf<double> dbox;  // lo, hi, plo, phi, box_lo, box_hi
-    DevBuf<unsigned long long> dhull, dflags;
     const size_t nb = 4 * n + 2 * (ni + 1);
     std::vector<double> hb(nb, 0.0);
     for (uint64_t i = 0; i < n; ++i) {
@@ -998,56 +1309,95 @@ pirk_status run_mc(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p, ui
         hb[4 * n + j] = p->input_lower[j];
         hb[4 * n + ni + 1 + j] = p->input_upper[j];
     }
-    CK(ctx, dbox.alloc(nb));
-    CK(ctx, dhull.alloc(S * 2 * n));
-    CK(ctx, dflags.alloc(2));
-    CK(ctx, cudaMemcpyAsync(dbox.p, hb.data(), nb * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-    for (uint64_t s = 0; s < S; ++s) {
-        CK(ctx, cudaMemsetAsync(dhull.p + s * 2 * n, 0xff, n * sizeof(unsigned long long), ctx->stream));
-        CK(ctx, cudaMemsetAsync(dhull.p + s * 2 * n + n, 0x00, n * sizeof(unsigned long long), ctx->stream));
-    }
-    CK(ctx, cudaMemsetAsync(dflags.p, 0xff, sizeof(unsigned long long), ctx->stream));
-    CK(ctx, cudaMemsetAsync(dflags.p + 1, 0x00, sizeof(unsigned long long), ctx->stream));
-    McArgs a{};
-    a.lo = dbox.p;
-    a.hi = dbox.p + n;
-    a.plo = dbox.p + 4 * n;
-    a.phi = dbox.p + 4 * n + ni + 1;
-    a.seed = seed;
-    a.s_begin = s_begin;
-    a.s_end = s_end;
-    a.t0 = p->t0;
-    a.t1 = p->t1;
-    a.h = p->h;
-    a.total = plan.total;
-    a.stride = coverage ? 0 : p->tube_stride;
-    a.slots = S;
-    a.hull = dhull.p;
-    a.fail = dflags.p;
-    if (coverage) {
-        a.box_lo = dbox.p + 2 * n;
-        a.box_hi = dbox.p + 3 * n;
-        a.outside = dflags.p + 1;
+    const uint64_t count = s_end - s_begin;
+    const int W = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(ctx->lanes()), count));
+    struct McLane {
+        LaneRef L{};
+        uint64_t sb = 0, se = 0;
+        DevBuf<double> dbox;  // lo, hi, box_lo, box_hi, plo, phi
+        DevBuf<unsigned long long> dhull, dflags;
+        std::vector<unsigned long long> hull;
+        unsigned long long fl[2] = {kNoFail, 0};
+    };
+    std::unique_ptr<McLane[]> ln(new McLane[static_cast<size_t>(W)]);
+    for (int r = 0; r < W; ++r) {
+        McLane& z = ln[static_cast<size_t>(r)];
+        z.L = lane_ref(ctx, r);
+        z.sb = s_begin + count * static_cast<uint64_t>(r) / static_cast<uint64_t>(W);
+        z.se = s_begin + count * static_cast<uint64_t>(r + 1) / static_cast<uint64_t>(W);
+        CK(ctx, cudaSetDevice(z.L.device));
+        CK(ctx, z.dbox.alloc(ctx, nb));
+        CK(ctx, z.dhull.alloc(ctx, S * 2 * n));
+        CK(ctx, z.dflags.alloc(ctx, 2));
+        CK(ctx, cudaMemcpyAsync(z.dbox.p, hb.data(), nb * sizeof(double), cudaMemcpyHostToDevice, z.L.s));
+        for (uint64_t s = 0; s < S; ++s) {  // hull init +inf / -inf as ordered keys (reach.cpp:218-221)
+            CK(ctx, cudaMemsetAsync(z.dhull.p + s * 2 * n, 0xff, n * sizeof(unsigned long long), z.L.s));
+            CK(ctx, cudaMemsetAsync(z.dhull.p + s * 2 * n + n, 0x00, n * sizeof(unsigned long long), z.L.s));
+        }
+        CK(ctx, cudaMemsetAsync(z.dflags.p, 0xff, sizeof(unsigned long long), z.L.s));
+        CK(ctx, cudaMemsetAsync(z.dflags.p + 1, 0x00, sizeof(unsigned long long), z.L.s));
     }
     const double setup_s = since(t_setup);
     const auto t_int = Clock::now();
-    CK(ctx, exact_mode(ctx) ? launch_monte_carlo<true>(sm, a, ctx->stream)
-                            : launch_monte_carlo<false>(sm, a, ctx->stream));
-    ctx->launches++;
-    std::vector<unsigned long long> hull(S * 2 * n);
-    unsigned long long fl[2];
-    CK(ctx, cudaMemcpyAsync(hull.data(), dhull.p, hull.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(ctx, cudaMemcpyAsync(fl, dflags.p, sizeof fl, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(ctx, cudaStreamSynchronize(ctx->stream));
+    for (int r = 0; r < W; ++r) {
+        McLane& z = ln[static_cast<size_t>(r)];
+        McArgs a{};
+        a.lo = z.dbox.p;
+        a.hi = z.dbox.p + n;
+        a.plo = z.dbox.p + 4 * n;
+        a.phi = z.dbox.p + 4 * n + ni + 1;
+        a.seed = seed;
+        a.s_begin = z.sb;
+        a.s_end = z.se;
+        a.t0 = p->t0;
+        a.t1 = p->t1;
+        a.h = p->h;
+        a.total = plan.total;
+        a.stride = coverage ? 0 : p->tube_stride;
+        a.slots = S;
+        a.hull = z.dhull.p;
+        a.fail = z.dflags.p;
+        if (coverage) {
+            a.box_lo = z.dbox.p + 2 * n;
+            a.box_hi = z.dbox.p + 3 * n;
+            a.outside = z.dflags.p + 1;
+        }
+        CK(ctx, cudaSetDevice(z.L.device));
+        CK(ctx, exact_mode(ctx) ? launch_monte_carlo<true>(sm, a, z.L.s)
+                                : launch_monte_carlo<false>(sm, a, z.L.s));
+        ctx->launches++;
+        z.hull.resize(S * 2 * n);
+        CK(ctx, cudaMemcpyAsync(z.hull.data(), z.dhull.p, z.hull.size() * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, z.L.s));
+        CK(ctx, cudaMemcpyAsync(z.fl, z.dflags.p, sizeof z.fl, cudaMemcpyDeviceToHost, z.L.s));
+    }
+    for (int r = 0; r < W; ++r) {
+        CK(ctx, cudaSetDevice(ln[static_cast<size_t>(r)].L.device));
+        CK(ctx, cudaStreamSynchronize(ln[static_cast<size_t>(r)].L.s));
+    }
+    CK(ctx, cudaSetDevice(ctx->device));
     const double integ_s = since(t_int);
     const auto t_red = Clock::now();
-    if (fl[0] != kNoFail) {
-        const uint64_t smp = s_begin + (fl[0] >> 30), st = (fl[0] >> 10) & 0xfffff, comp = fl[0] & 0x3ff;
-        return fail(ctx, PIRK_EINTEGRATION, "monte-carlo sample " + std::to_string(smp) + " integration: " +
-                                                integ_msg(st, comp, p->t0 + static_cast<double>(st) * p->h));
+    // the lowest failing sample over all lanes (its lane's key is lane-relative)
+    uint64_t fail_sample = ~0ull, fail_step = 0, fail_comp = 0;
+    unsigned long long outside = 0;
+    for (int r = 0; r < W; ++r) {
+        const McLane& z = ln[static_cast<size_t>(r)];
+        if (z.fl[0] != kNoFail) {
+            const uint64_t smp = z.sb + (z.fl[0] >> 30);
+            if (smp < fail_sample) {
+                fail_sample = smp;
+                fail_step = (z.fl[0] >> 10) & 0xfffff;
+                fail_comp = z.fl[0] & 0x3ff;
+            }
+        }
+        outside += z.fl[1];
     }
+    if (fail_sample != ~0ull)
+        return fail(ctx, PIRK_EINTEGRATION, "monte-carlo sample " + std::to_string(fail_sample) + " integration: " +
+                                                integ_msg(fail_step, fail_comp, p->t0 + static_cast<double>(fail_step) * p->h));
     if (coverage) {
-        *fraction = static_cast<double>(fl[1]) / static_cast<double>(s_end - s_begin);
+        *fraction = static_cast<double>(outside) / static_cast<double>(count);
         return PIRK_OK;
     }
     if (tube) {
@@ -1055,8 +1405,13 @@ pirk_status run_mc(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p, ui
         for (uint64_t s = 0; s < S; ++s) {
             if (tube->times) tube->times[s] = slot_times[s];
             for (uint64_t i = 0; i < n; ++i) {
-                const double lo = ord_val(hull[s * 2 * n + i]);
-                const double hi = ord_val(hull[s * 2 * n + n + i]);
+                unsigned long long klo = ln[0].hull[s * 2 * n + i], khi = ln[0].hull[s * 2 * n + n + i];
+                for (int r = 1; r < W; ++r) {  // HullAccumulator::merge (reach.cpp:232-241) on keys
+                    klo = std::min(klo, ln[static_cast<size_t>(r)].hull[s * 2 * n + i]);
+                    khi = std::max(khi, ln[static_cast<size_t>(r)].hull[s * 2 * n + n + i]);
+                }
+                const double lo = ord_val(klo);
+                const double hi = ord_val(khi);
                 if (fold_into) {
                     if (tube->lower && lo < tube->lower[s * n + i]) tube->lower[s * n + i] = lo;
                     if (tube->upper && hi > tube->upper[s * n + i]) tube->upper[s * n + i] = hi;
@@ -1067,10 +1422,12 @@ pirk_status run_mc(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p, ui
             }
         }
     }
-    // reach.cpp:273-275 with one worker
-    const uint64_t peak = (7 * n * sizeof(double) + 2 * S * n * sizeof(double)) + 2 * S * n * sizeof(double);
-    fill_report(rep, n, m_total, plan.total, peak, nb * sizeof(double) + S * 2 * n * 8,
+    // reach.cpp:273-275 with `outer` = lanes
+    const uint64_t peak = static_cast<uint64_t>(W) * (7 * n * sizeof(double) + 2 * S * n * sizeof(double)) +
+                          2 * S * n * sizeof(double);
+    fill_report(rep, n, m_total, plan.total, peak, static_cast<uint64_t>(W) * (nb * sizeof(double) + S * 2 * n * 8),
                 exact_mode(ctx), setup_s, integ_s, since(t_red), ctx->launches - launches0);
+    if (rep) rep->workers = W;
     return PIRK_OK;
 }
 
@@ -1082,35 +1439,100 @@ extern "C" {
 
 int32_t pirk_abi_version(void) { return PIRK_ABI_VERSION; }
 
-pirk_status pirk_create(int device, pirk_ctx** out) {
-    if (!out) return PIRK_EINVAL;
+pirk_status pirk_create(int device, pirk_ctx** out) { return pirk_create_multi(1, &device, out); }
+
+pirk_status pirk_create_multi(int n_lanes, const int* devices, pirk_ctx** out) {
+    if (!out || n_lanes < 1 || !devices) return PIRK_EINVAL;
     *out = nullptr;
     int count = 0;
     cudaError_t e = cudaGetDeviceCount(&count);
     if (e != cudaSuccess || count == 0) return PIRK_ECUDA;
-    if (device < 0 || device >= count) return PIRK_EINVAL;
+    for (int r = 0; r < n_lanes; ++r)
+        if (devices[r] < 0 || devices[r] >= count) return PIRK_EINVAL;
     pirk_ctx* ctx = new (std::nothrow) pirk_ctx;
     if (!ctx) return PIRK_ENOMEM;
+    const int device = devices[0];
     ctx->device = device;
     if (cudaSetDevice(device) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->own_xstream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMalloc(reinterpret_cast<void**>(&ctx->d_flags), 16 * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMallocHost(reinterpret_cast<void**>(&ctx->h_flags), 16 * sizeof(unsigned long long)) != cudaSuccess) {
-        delete ctx;
+        pirk_destroy(ctx);
         return PIRK_ECUDA;
     }
     ctx->stream = ctx->own_stream;
+    for (int r = 1; r < n_lanes; ++r) {
+        PirkLane l;
+        l.device = devices[r];
+        ctx->peers.push_back(l);
+        PirkLane& lr = ctx->peers.back();
+        if (cudaSetDevice(lr.device) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&lr.stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&lr.xstream, cudaStreamNonBlocking) != cudaSuccess) {
+            pirk_destroy(ctx);
+            return PIRK_ECUDA;
+        }
+    }
+    // halos move between adjacent lanes: direct NVLink peer access where the
+    // devices differ (cudaMemcpyPeerAsync falls back to staging otherwise)
+    for (int r = 0; r + 1 < n_lanes; ++r) {
+        const int a = devices[r], b = devices[r + 1];
+        if (a == b) continue;
+        for (int dir = 0; dir < 2; ++dir) {
+            const int from = dir ? b : a, to = dir ? a : b;
+            int ok = 0;
+            if (cudaDeviceCanAccessPeer(&ok, from, to) == cudaSuccess && ok) {
+                cudaSetDevice(from);
+                const cudaError_t pe = cudaDeviceEnablePeerAccess(to, 0);
+                if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            }
+        }
+    }
+    cudaSetDevice(device);
     *out = ctx;
+    return PIRK_OK;
+}
+
+int32_t pirk_lane_count(const pirk_ctx* ctx) { return ctx ? ctx->lanes() : 0; }
+
+int32_t pirk_device_count(void) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return count;
+}
+
+int32_t pirk_lane_device(const pirk_ctx* ctx, int32_t lane) {
+    if (!ctx || lane < 0 || lane >= ctx->lanes()) return -1;
+    return lane == 0 ? ctx->device : ctx->peers[static_cast<size_t>(lane - 1)].device;
+}
+
+pirk_status pirk_release_cache(pirk_ctx* ctx) {
+    if (!ctx) return PIRK_EINVAL;
+    LOCK(ctx);
+    ctx->flush_all();
     return PIRK_OK;
 }
 
 void pirk_destroy(pirk_ctx* ctx) {
     if (!ctx) return;
-    cudaSetDevice(ctx->device);
-    ctx->flush_cache();
-    if (ctx->d_flags) cudaFree(ctx->d_flags);
-    if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
-    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    {
+        LOCK(ctx);
+        ctx->flush_all();
+        for (PirkLane& l : ctx->peers) {
+            cudaSetDevice(l.device);
+            if (l.stream) cudaStreamDestroy(l.stream);
+            if (l.xstream) cudaStreamDestroy(l.xstream);
+        }
+        cudaSetDevice(ctx->device);
+        if (ctx->d_flags) cudaFree(ctx->d_flags);
+        if (ctx->h_flags) cudaFreeHost(ctx->h_flags);
+        if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+        if (ctx->own_xstream) cudaStreamDestroy(ctx->own_xstream);
+    }
     delete ctx;
 }
 
@@ -1118,12 +1540,14 @@ const char* pirk_last_error(const pirk_ctx* ctx) { return ctx ? ctx->err.c_str()
 
 pirk_status pirk_set_mode(pirk_ctx* ctx, int32_t mode) {
     if (!ctx || (mode != PIRK_MODE_EXACT && mode != PIRK_MODE_FAST)) return PIRK_EINVAL;
+    LOCK(ctx);
     ctx->mode = mode;
     return PIRK_OK;
 }
 
 pirk_status pirk_set_stream(pirk_ctx* ctx, void* stream) {
     if (!ctx) return PIRK_EINVAL;
+    LOCK(ctx);
     ctx->stream = static_cast<cudaStream_t>(stream);  // NULL = the CUDA default stream
     return PIRK_OK;
 }
@@ -1184,6 +1608,7 @@ int32_t pirk_supports(const pirk_model* m, int32_t method) {
 static pirk_status reach_mm_gb(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p,
                                pirk_tube* tube, pirk_report* rep, int method) {
     if (!ctx) return PIRK_EINVAL;
+    LOCK(ctx);
     ctx->err.clear();
     if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, PIRK_ECUDA, "cudaSetDevice failed");
     pirk_status st = PIRK_OK;
@@ -1200,7 +1625,10 @@ static pirk_status reach_mm_gb(pirk_ctx* ctx, const pirk_model* m, const pirk_pr
             return fail(ctx, PIRK_EUNSUPPORTED, "growth_bound: no device kernel for this model");
     }
     try {
-        return large ? run_large(ctx, m, method, p, tube, rep) : run_small(ctx, m, method, p, tube, rep);
+        if (!large) return run_small(ctx, m, method, p, tube, rep);
+        if (ctx->lanes() > 1 && usable_lanes(ctx, is_heat(m) ? m->grid : m->dim) > 1)
+            return run_large_multi(ctx, m, method, p, tube, rep);
+        return run_large(ctx, m, method, p, tube, rep);
     } catch (const std::bad_alloc&) {
         return fail(ctx, PIRK_ENOMEM, "host allocation failed");
     }
@@ -1220,6 +1648,7 @@ pirk_status pirk_growth_bound(pirk_ctx* ctx, const pirk_model* model, const pirk
 pirk_status pirk_monte_carlo(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p,
                              const pirk_mc_spec* spec, pirk_tube* tube, pirk_report* report) {
     if (!ctx || !spec) return PIRK_EINVAL;
+    LOCK(ctx);
     ctx->err.clear();
     if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, PIRK_ECUDA, "cudaSetDevice failed");
     pirk_status st = PIRK_OK;
@@ -1243,6 +1672,7 @@ pirk_status pirk_monte_carlo_range(pirk_ctx* ctx, const pirk_model* m, const pir
                                    uint64_t seed, uint64_t s_begin, uint64_t s_end,
                                    pirk_tube* tube, pirk_report* report) {
     if (!ctx) return PIRK_EINVAL;
+    LOCK(ctx);
     ctx->err.clear();
     if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, PIRK_ECUDA, "cudaSetDevice failed");
     pirk_status st = PIRK_OK;
@@ -1263,6 +1693,7 @@ pirk_status pirk_coverage_estimate(pirk_ctx* ctx, const pirk_model* m, const pir
                                    const double* box_lower, const double* box_upper,
                                    uint64_t fresh_samples, uint64_t seed, double* fraction) {
     if (!ctx || !fraction) return PIRK_EINVAL;
+    LOCK(ctx);
     ctx->err.clear();
     pirk_status st = PIRK_OK;
     if (!check_problem(ctx, m, p, true, st)) return st;
@@ -1279,6 +1710,7 @@ pirk_status pirk_coverage_estimate(pirk_ctx* ctx, const pirk_model* m, const pir
 pirk_status pirk_engine_create(pirk_ctx* ctx, const pirk_model* m, int32_t method,
                                const pirk_problem* p, pirk_engine** out) {
     if (!ctx || !out) return PIRK_EINVAL;
+    LOCK(ctx);
     *out = nullptr;
     ctx->err.clear();
     if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, PIRK_ECUDA, "cudaSetDevice failed");
@@ -1299,11 +1731,13 @@ pirk_status pirk_engine_create(pirk_ctx* ctx, const pirk_model* m, int32_t metho
 
 pirk_status pirk_engine_advance(pirk_engine* e, uint64_t nsteps) {
     if (!e) return PIRK_EINVAL;
+    LOCK(e->ctx);
     return engine_advance(e, nsteps);
 }
 
 pirk_status pirk_engine_status(pirk_engine* e, uint64_t* steps_done) {
     if (!e) return PIRK_EINVAL;
+    LOCK(e->ctx);
     pirk_ctx* ctx = e->ctx;
     unsigned long long f[2];
     CK(ctx, cudaMemcpyAsync(f, e->d_fail.p, sizeof f, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1320,6 +1754,7 @@ pirk_status pirk_engine_status(pirk_engine* e, uint64_t* steps_done) {
 
 pirk_status pirk_engine_read(pirk_engine* e, double* lower, double* upper) {
     if (!e) return PIRK_EINVAL;
+    LOCK(e->ctx);
     pirk_ctx* ctx = e->ctx;
     const uint64_t n = e->n;
     const double* lo = e->s0();
@@ -1337,12 +1772,17 @@ pirk_status pirk_engine_read(pirk_engine* e, double* lower, double* upper) {
     return PIRK_OK;
 }
 
-void pirk_engine_destroy(pirk_engine* e) { delete e; }
+void pirk_engine_destroy(pirk_engine* e) {
+    if (!e) return;
+    std::lock_guard<std::recursive_mutex> lk(e->ctx->mu);
+    delete e;
+}
 
 pirk_status pirk_step_window(pirk_ctx* ctx, const pirk_model* m, int32_t method,
                              const pirk_window* win, const double* p0, const double* p1,
                              double t, double hk, uint64_t step_index, uint64_t* fail_ptr) {
     if (!ctx || !win) return PIRK_EINVAL;
+    LOCK(ctx);
     pirk_status st = PIRK_OK;
     if (!check_model(ctx, m, st)) return st;
     if (!(is_chain(m) || is_heat(m)) || !pirk_supports(m, method))
@@ -1370,7 +1810,7 @@ pirk_status pirk_step_window(pirk_ctx* ctx, const pirk_model* m, int32_t method,
     const ChainModel cm = chain_model(m, method, q0, q1);
     const HeatModel hm = heat_model(m, method);
     WindowArgs w{win->in0, win->in1, win->out0, win->out1, wb, we, win->out_begin, win->out_end};
-    CK(ctx, step_launch(ctx, m, method, cm, hm, w, sc, step_index,
+    CK(ctx, step_launch(ctx, ctx->stream, m, cm, hm, w, sc, step_index,
                         reinterpret_cast<unsigned long long*>(fail_ptr)));
     return PIRK_OK;
 }

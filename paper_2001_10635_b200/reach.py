@@ -210,20 +210,35 @@ _EXC = {
 
 
 class Context:
-    """A pirk_ctx: one device, one stream, one arithmetic mode.  Not
-    reentrant (like ivreach::Rk4Engine)."""
+    """A pirk_ctx: one arithmetic mode and one or more shard lanes (device +
+    streams).  ``Context(0)`` is one lane on cuda:0; ``Context(devices=[0, 1,
+    2, 3])`` shards chain / heat3d runs across four lanes (z-slabs / index
+    ranges with NVLink halo copies) and Monte Carlo runs across their sample
+    ranges -- bit-identical to one lane.  Device ids may repeat (lanes then
+    share a GPU).  Calls on one context serialise on its mutex."""
 
-    def __init__(self, device: int = 0, mode: str = "exact"):
+    def __init__(self, device: int = 0, mode: str = "exact", devices=None):
         L = _lib.lib()
         h = C.c_void_p()
-        st = L.pirk_create(int(device), C.byref(h))
+        devs = [int(device)] if devices is None else [int(d) for d in devices]
+        arr = (C.c_int * len(devs))(*devs)
+        st = L.pirk_create_multi(len(devs), arr, C.byref(h))
         if st != _lib.OK:
-            raise RuntimeError(f"pirk_create(device={device}) failed with status {st} "
+            raise RuntimeError(f"pirk_create(devices={devs}) failed with status {st} "
                                "(no CUDA device?)")
         self._h = h
-        self.device = int(device)
+        self.device = devs[0]
+        self.devices = devs
         self._own_stream = L.pirk_get_stream(h)
         self.set_mode(mode)
+
+    @property
+    def lanes(self) -> int:
+        return int(_lib.lib().pirk_lane_count(self._h))
+
+    def release_cache(self) -> None:
+        """Free the state buffers kept for the next run of the same size."""
+        self.check(_lib.lib().pirk_release_cache(self._h))
 
     @property
     def handle(self):
@@ -282,6 +297,31 @@ def get_context(device: int = 0) -> Context:
         if ctx is None:
             ctx = Context(device)
             _contexts[device] = ctx
+    if ctx.mode != _default_mode:
+        ctx.set_mode(_default_mode)
+    return ctx
+
+
+def lanes_for_workers(workers: int):
+    """The reference's `workers` (reach.hpp:48,53,70) -> shard lanes: `workers`
+    lanes spread round-robin over the visible GPUs (workers == device count
+    puts one shard on each GPU)."""
+    count = int(_lib.lib().pirk_device_count())
+    if count == 0:
+        raise RuntimeError("no CUDA device: the PIRK device library has no CPU fallback")
+    return [r % count for r in range(int(workers))]
+
+
+def get_worker_context(workers: int) -> Context:
+    """Process-wide context for `workers` lanes (workers == 1: get_context())."""
+    if workers <= 1:
+        return get_context()
+    with _ctx_lock:
+        key = ("workers", int(workers))
+        ctx = _contexts.get(key)
+        if ctx is None:
+            ctx = Context(devices=lanes_for_workers(workers))
+            _contexts[key] = ctx
     if ctx.mode != _default_mode:
         ctx.set_mode(_default_mode)
     return ctx
@@ -381,7 +421,7 @@ def _run_tube(fn_name: str, method: str, problem: ReachProblem, workers: int, ct
     validate(problem)
     if workers < 1:
         raise ValueError(f"{method.replace('-', '_')}: workers must be >= 1")
-    ctx = ctx or get_context()
+    ctx = ctx or get_worker_context(workers)
     mar = _Marshalled(problem)
     n = problem.model.dim
     _, times = record_schedule(problem.t0, problem.t1, problem.h, problem.tube_stride)

@@ -139,7 +139,9 @@ class HaloExchanger:
 
 
 def device_step_fn(model: SystemModel, method: str, ctx=None):
-    """Windowed RK4 step on the B200 (pirk_step_window on torch tensors)."""
+    """Windowed RK4 step on the B200 (pirk_step_window on torch tensors), on
+    torch's current stream; the context's own stream is restored afterwards."""
+    from . import _lib
     from .reach import get_context, step_window
 
     ctx = ctx or get_context()
@@ -148,14 +150,40 @@ def device_step_fn(model: SystemModel, method: str, ctx=None):
              fail_ptr=0):
         import torch
 
+        prev = _lib.lib().pirk_get_stream(ctx.handle)
         ctx.set_stream(torch.cuda.current_stream().cuda_stream)
-        # out pointers address unit out_begin inside the window buffers
-        unit = units_of(model)[1]
-        off = (out_begin - win_begin) * unit * 8
-        step_window(model, method, in0.data_ptr(), in1.data_ptr(), out0.data_ptr() + off,
-                    out1.data_ptr() + off, win_begin, win_len, out_begin, out_end, p0, p1, t, hk,
-                    k, fail_ptr, ctx=ctx)
+        try:
+            # out pointers address unit out_begin inside the window buffers
+            unit = units_of(model)[1]
+            off = (out_begin - win_begin) * unit * 8
+            step_window(model, method, in0.data_ptr(), in1.data_ptr(), out0.data_ptr() + off,
+                        out1.data_ptr() + off, win_begin, win_len, out_begin, out_end, p0, p1, t,
+                        hk, k, fail_ptr, ctx=ctx)
+        finally:
+            ctx.set_stream(prev or 0)
     return step
+
+
+NO_FAIL = (1 << 64) - 1
+FAIL_COMP_BITS = 40  # csrc/common.cuh kFailCompBits
+
+
+def failure_message(method: str, keys, t0: float, h: float):
+    """The reference's IntegrationError text (rk4.cpp:19-23 wrapped as in
+    reach.cpp:107-117 / :190-192) for the minimum device failure keys
+    ``keys`` = (field 0, field 1) -- or None when no step failed."""
+    def one(key):
+        step, comp = key >> FAIL_COMP_BITS, key & ((1 << FAIL_COMP_BITS) - 1)
+        return (f"integration produced a non-finite value at step {step}, component {comp}, "
+                f"t = {t0 + float(step) * h:f}")
+    if method == "mixed-monotonicity":
+        k = min(keys)
+        return None if k == NO_FAIL else "mixed-monotonicity embedding integration: " + one(k)
+    if keys[0] != NO_FAIL:
+        return "growth-bound center integration: " + one(keys[0])
+    if keys[1] != NO_FAIL:
+        return "growth-bound radius integration: " + one(keys[1])
+    return None
 
 
 class ShardedReach:
@@ -175,11 +203,39 @@ class ShardedReach:
         self.K = K
         self.unit = units_of(model)[1]
 
-    def alloc(self, like_tensor_factory):
+    def alloc(self, like_tensor_factory, fail=None):
+        """Window buffers from ``like_tensor_factory(n)``; ``fail`` is an
+        optional device tensor of two uint64 failure keys (all ones = none)
+        that every step's kernels atomically lower (see check())."""
         n = self.shard.win_len * self.unit
         self.a = [like_tensor_factory(n), like_tensor_factory(n)]
         self.b = [like_tensor_factory(n), like_tensor_factory(n)]
+        self.fail = fail
         return self.a
+
+    def _fail_ptr(self):
+        f = getattr(self, "fail", None)
+        return 0 if f is None else f.data_ptr()
+
+    def check(self, t0: float, h: float, group=None):
+        """Raise the reference's IntegrationError (as RuntimeError) if any rank's
+        kernels saw a non-finite value: the per-rank minimum keys are combined
+        with a MIN all-reduce, so every rank raises the same message."""
+        f = getattr(self, "fail", None)
+        if f is None:
+            return
+        import torch
+
+        v = f.view(torch.int64).clone()
+        big = torch.iinfo(torch.int64).max
+        v = torch.where(v == -1, torch.full_like(v, big), v)  # no failure -> +inf
+        import torch.distributed as dist
+        if self.shard.world > 1 and dist.is_available() and dist.is_initialized():
+            dist.all_reduce(v, op=dist.ReduceOp.MIN, group=group)
+        keys = [NO_FAIL if int(x) == big else int(x) for x in v.cpu().tolist()]
+        msg = failure_message(self.method, keys, t0, h)
+        if msg:
+            raise RuntimeError(msg)
 
     def run(self, steps, k0: int = 0, overlap: bool = True):
         """steps: list of (t, hk) for global step indices k0, k0+1, ...
@@ -190,6 +246,7 @@ class ShardedReach:
         the halos have landed.  Every unit is still computed once, from the
         same inputs, so results do not depend on ``overlap``."""
         s = self.shard
+        fp = self._fail_ptr()
         for i, (t, hk) in enumerate(steps):
             sub = (k0 + i) % self.K
             lo, hi = s.out_range(sub)
@@ -200,17 +257,17 @@ class ShardedReach:
                     ilo, ihi = max(lo, s.begin + 4), min(hi, s.end - 4)
                     if ilo < ihi:  # interior: independent of the incoming halos
                         self.step_fn(self.a[0], self.a[1], self.b[0], self.b[1], *args, ilo, ihi,
-                                     self.p0, self.p1, t, hk, k0 + i)
+                                     self.p0, self.p1, t, hk, k0 + i, fp)
                     self.ex.finish(handle)
                     for blo, bhi in ((lo, min(hi, ilo)), (max(lo, ihi), hi)) if ilo < ihi else ((lo, hi),):
                         if blo < bhi:
                             self.step_fn(self.a[0], self.a[1], self.b[0], self.b[1], *args, blo, bhi,
-                                         self.p0, self.p1, t, hk, k0 + i)
+                                         self.p0, self.p1, t, hk, k0 + i, fp)
                     self.a, self.b = self.b, self.a
                     continue
                 self.ex.exchange(self.a)
             self.step_fn(self.a[0], self.a[1], self.b[0], self.b[1], *args, lo, hi, self.p0, self.p1, t,
-                         hk, k0 + i)
+                         hk, k0 + i, fp)
             self.a, self.b = self.b, self.a
 
     def owned(self):

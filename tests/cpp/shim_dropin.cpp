@@ -78,5 +78,43 @@ int main(int argc, char** argv) {
         try { dispatch("bogus", p, MonteCarloSpec{}, 1); } catch (const std::invalid_argument&) { threw = true; }
         check(threw, "dispatch: unknown method -> invalid_argument");
     }
+    {   // workers -> shard lanes (ivreach_gpu::Device::current(workers)): the
+        // sharded run is bit-identical to one lane
+        const std::size_t n = 1000000;
+        ReachProblem p{make_traffic(n), IntervalVector(std::vector<double>(n, 10.0), std::vector<double>(n, 20.0)),
+                       IntervalVector({4.0}, {6.0}), 0.0, 30.0, 0.5, 10};
+        const ReachTube one = mixed_monotonicity(p, 1), three = mixed_monotonicity(p, 3);
+        bool same = one.entries.size() == three.entries.size();
+        for (std::size_t s = 0; same && s < one.entries.size(); ++s)
+            same = one.entries[s].t == three.entries[s].t && one.entries[s].box == three.entries[s].box;
+        check(same, "traffic n=1e6 CTMM: mixed_monotonicity(p, 3) == mixed_monotonicity(p, 1)");
+        const IntervalVector& fin = three.entries.back().box;
+        check(fin.lower(0) == 8.4261226388996242 && fin.lower(n - 1) == 8.8249690258461371,
+              "3-lane traffic CTMM bit-identical to the reference golden values");
+        check(three.report.workers == 3, "report.workers == 3");
+        const ReachTube g1 = growth_bound(p, 1), g3 = growth_bound(p, 3);
+        check(g1.entries.back().box == g3.entries.back().box, "traffic GB: workers 3 == workers 1");
+    }
+    {   // heat3d z-slabs over 3 lanes
+        const std::size_t g = 40, n = g * g * g;
+        std::vector<double> lo(n), hi(n);
+        for (std::size_t i = 0; i < n; ++i) { lo[i] = 0.9 + 0.001 * static_cast<double>(i % 13); hi[i] = lo[i] + 0.2; }
+        const double h = 0.2 / 39.0 / 39.0;
+        ReachProblem p{make_heat3d(g), IntervalVector(lo, hi), std::nullopt, 0.0, 6 * h, h, 2};
+        const ReachTube a = mixed_monotonicity(p, 1), b = mixed_monotonicity(p, 3);
+        bool same = a.entries.size() == b.entries.size();
+        for (std::size_t s = 0; same && s < a.entries.size(); ++s) same = a.entries[s].box == b.entries[s].box;
+        check(same, "heat3d g=40 CTMM: workers 3 == workers 1");
+    }
+    {   // Monte Carlo sample ranges over 3 lanes, hull folded exactly
+        ReachProblem p{make_laub_loomis(), IntervalVector({1.15, 1.0, 1.45, 2.35, 0.95, 0.05, 0.4},
+                                                          {1.25, 1.1, 1.55, 2.45, 1.05, 0.15, 0.5}),
+                       std::nullopt, 0.0, 1.0, 0.01, 10};
+        MonteCarloSpec s; s.seed = 3; s.samples_override = 10007;
+        const ReachTube a = monte_carlo(p, s, 1), b = monte_carlo(p, s, 3);
+        bool same = a.entries.size() == b.entries.size();
+        for (std::size_t k = 0; same && k < a.entries.size(); ++k) same = a.entries[k].box == b.entries[k].box;
+        check(same, "laub-loomis MC: workers 3 == workers 1");
+    }
     return failures;
 }

@@ -32,7 +32,7 @@ def oracle_step_fn(model, method):
     meth = 0 if method == "mixed-monotonicity" else 1
     unit = S.units_of(model)[1]
 
-    def step(in0, in1, out0, out1, wb, wl, lo, hi, p0, p1, t, hk, k):
+    def step(in0, in1, out0, out1, wb, wl, lo, hi, p0, p1, t, hk, k, fail_ptr=0):
         o0, o1 = O.step_window(model, meth, in0.numpy(), in1.numpy(), wb, wl, lo, hi, p0, p1, t,
                                hk)
         a = (lo - wb) * unit
