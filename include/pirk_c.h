@@ -66,7 +66,8 @@ typedef enum pirk_model_kind {
     PIRK_CHAIN = 5,         /* synthetic coupled chain (a, b, c)  */
     PIRK_LAUB_LOOMIS = 6,   /* make_laub_loomis()                   models.cpp:463-502 */
     PIRK_ARCH_QUAD = 7,     /* make_arch_quadrotor(mass,g,jx,jy,jz) models.cpp:504-613 */
-    PIRK_VDP = 8            /* make_vdp(mu, op_x, op_y)             models.cpp:444-461 */
+    PIRK_VDP = 8,           /* make_vdp(mu, op_x, op_y)             models.cpp:444-461 */
+    PIRK_USER = 9           /* user-defined evaluators: pirk_model.program            */
 } pirk_model_kind;
 
 typedef enum pirk_decomp {
@@ -75,6 +76,8 @@ typedef enum pirk_decomp {
     PIRK_DECOMP_JACOBIAN = 2  /* d_i = f_i(x) + sum_{j!=i,C_ij!=0} C_ij (x_j - xh_j), C = growth matrix */
 } pirk_decomp;
 
+typedef struct pirk_program pirk_program;
+
 typedef struct pirk_model {
     int32_t kind;        /* pirk_model_kind */
     int32_t decomp;      /* pirk_decomp */
@@ -82,7 +85,38 @@ typedef struct pirk_model {
     uint64_t input_dim;
     uint64_t grid;       /* heat3d nodes per axis, else 0 */
     double params[8];    /* kind-specific, in make_* argument order */
+    const pirk_program* program;  /* PIRK_USER: the compiled evaluators, else NULL */
 } pirk_model;
+
+/* ---- user-defined models (the reference's SystemModel with arbitrary
+ * std::function evaluators, system_model.hpp:14-43) ----
+ * `source` is CUDA C++ defining, as the flags say,
+ *   __device__ double pirk_rhs(u64 i, double t, const double* x, const double* p);
+ *   __device__ double pirk_decomposition(u64 i, double t, const double* x, const double* p,
+ *                                        const double* xh, const double* ph);
+ *   __device__ double pirk_growth(u64 i, double t, const double* r, const double* w);
+ * (u64 = unsigned long long; PIRK_N / PIRK_NI = dim / input_dim; pirk_min /
+ * pirk_max = std::min / std::max).  It is compiled with NVRTC for sm_100a on
+ * first use in each arithmetic mode (exact: --fmad=false, so +,-,*,/ round
+ * like the reference's build).  Use it through a pirk_model with kind
+ * PIRK_USER, dim / input_dim equal to the program's, and .program set; every
+ * entry point accepts it (MM / GB: one device thread per integration for
+ * n <= 64, else one thread per component and stage; MC: n <= 1024). */
+enum {
+    PIRK_HAS_RHS = 1,
+    PIRK_HAS_DECOMPOSITION = 2,
+    PIRK_HAS_GROWTH = 4,
+    PIRK_INPUT_AFFINE = 8      /* SystemModel::input_affine (growth bound needs it) */
+};
+pirk_status pirk_program_create(const char* source, uint64_t dim, uint64_t input_dim, uint32_t flags,
+                                pirk_program** out);
+/* Compile now (no device needed) in `mode`; on failure log receives the NVRTC
+ * log.  *cubin_bytes (may be NULL) receives the size of the sm_100a image. */
+pirk_status pirk_program_compile(pirk_program* prog, int32_t mode, char* log, size_t log_len,
+                                 uint64_t* cubin_bytes);
+/* Copy the compiled sm_100a cubin of `mode` (after pirk_program_compile). */
+pirk_status pirk_program_cubin(const pirk_program* prog, int32_t mode, void* buf, uint64_t len);
+void pirk_program_destroy(pirk_program* prog);
 
 /* ReachProblem (system_model.hpp:47-55). inputs may be NULL iff input_dim == 0. */
 typedef struct pirk_problem {

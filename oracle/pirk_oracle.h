@@ -36,7 +36,14 @@ enum {
     PO_CHAIN = 5,         /* SURVEY.md 8d C4      params: a, b, c                    */
     PO_LAUB_LOOMIS = 6,   /* models.cpp:463-502   params: -                          */
     PO_ARCH_QUAD = 7,     /* models.cpp:504-613   params: mass, gravity, jx, jy, jz  */
-    PO_VDP = 8            /* models.cpp:444-461   params: mu, op_x, op_y             */
+    PO_VDP = 8,           /* models.cpp:444-461   params: mu, op_x, op_y             */
+    /* User-defined systems of the reference's own tests, built from the same
+     * lambdas by oracle/ref_shim.cpp only (the device runs them as NVRTC user
+     * models, tests/test_gpu_user.py). */
+    PO_T_ORDER = 100,     /* test_reach.cpp:190-206: f = (x1, -1), d = (xh1, -1)     */
+    PO_T_EMBED = 101,     /* test_system_model.cpp:74-96: f = -x0, d = -xh0          */
+    PO_T_DRIFT = 102,     /* test_reach.cpp:208-230: make_zero(1), growth = params[0] */
+    PO_T_BARE = 103       /* test_reach.cpp:176-188: rhs = -x0 only                  */
 };
 
 /* Decomposition variants. */

@@ -96,6 +96,37 @@ SystemModel build_model(const po_model* pm) {
         case PO_LAUB_LOOMIS: m = make_laub_loomis(); break;
         case PO_ARCH_QUAD: m = make_arch_quadrotor(P[0], P[1], P[2], P[3], P[4]); break;
         case PO_VDP: m = make_vdp(P[0], P[1], P[2]); break;
+        case PO_T_ORDER:  // test_reach.cpp:190-206, verbatim lambdas
+            m.dim = 2;
+            m.input_dim = 0;
+            m.rhs = [](std::size_t i, double, std::span<const double> x,
+                       std::span<const double>) { return i == 0 ? x[1] : -1.0; };
+            m.decomposition = [](std::size_t i, double, std::span<const double>,
+                                 std::span<const double>, std::span<const double> xh,
+                                 std::span<const double>) { return i == 0 ? xh[1] : -1.0; };
+            return m;
+        case PO_T_EMBED:  // test_system_model.cpp:74-96
+            m.dim = 1;
+            m.input_dim = 0;
+            m.rhs = [](std::size_t, double, std::span<const double> x,
+                       std::span<const double>) { return -x[0]; };
+            m.decomposition = [](std::size_t, double, std::span<const double>,
+                                 std::span<const double>, std::span<const double> xh,
+                                 std::span<const double>) { return -xh[0]; };
+            return m;
+        case PO_T_DRIFT: {  // test_reach.cpp:208-230
+            m = make_zero(1);
+            const double g = P[0];
+            m.growth_rhs = [g](std::size_t, double, std::span<const double>,
+                               std::span<const double>) { return g; };
+            return m;
+        }
+        case PO_T_BARE:  // test_reach.cpp:176-188
+            m.dim = 1;
+            m.input_dim = 0;
+            m.rhs = [](std::size_t, double, std::span<const double> x,
+                       std::span<const double>) { return -x[0]; };
+            return m;
         default: throw std::invalid_argument("ref_shim: unknown model kind");
     }
     if (pm->decomp == PO_DECOMP_JACOBIAN) add_jacobian_decomposition(m);

@@ -30,6 +30,7 @@ class PirkModel(C.Structure):
         ("input_dim", C.c_uint64),
         ("grid", C.c_uint64),
         ("params", C.c_double * 8),
+        ("program", C.c_void_p),
     ]
 
 
@@ -133,6 +134,11 @@ SIGNATURES = {
     "pirk_engine_status": (C.c_int, [C.c_void_p, _U64P]),
     "pirk_engine_read": (C.c_int, [C.c_void_p, _DP, _DP]),
     "pirk_engine_destroy": (None, [C.c_void_p]),
+    "pirk_program_create": (C.c_int, [C.c_char_p, C.c_uint64, C.c_uint64, C.c_uint32,
+                                      C.POINTER(C.c_void_p)]),
+    "pirk_program_compile": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_size_t, _U64P]),
+    "pirk_program_cubin": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_uint64]),
+    "pirk_program_destroy": (None, [C.c_void_p]),
     "pirk_step_window": (C.c_int, [C.c_void_p, _MP, C.c_int32, C.POINTER(PirkWindow), _DP, _DP,
                                    C.c_double, C.c_double, C.c_uint64, C.c_void_p]),
 }

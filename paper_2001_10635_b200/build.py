@@ -69,8 +69,9 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
             sys.stderr.write(log)
     objs = [o for o, _ in results]
     tmp = out + ".tmp"
+    # NVRTC compiles user-defined models at run time (csrc/user_models.cuh)
     cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-ccbin", "/usr/bin/g++", *objs,
-           "-o", tmp]
+           "-lnvrtc", "-Xlinker", "-rpath=/usr/local/cuda/lib64", "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -9,6 +9,7 @@
 // transfers and formats.  There is no CPU fallback: an unsupported model or
 // a missing device is an error.
 #include <cuda_runtime.h>
+#include <nvrtc.h>
 
 #include <chrono>
 #include <cmath>
@@ -16,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <new>
@@ -26,8 +28,32 @@
 #include "../../include/pirk_c.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "user_rt.cuh"
 
 using namespace pirk;
+
+// A user-defined model's evaluators (pirk_program_create): source, and per
+// arithmetic mode the NVRTC-compiled sm_100a image loaded as a
+// context-independent library (user_models.cuh).
+struct UserBuild {
+    bool tried = false, ok = false;
+    std::string log;
+    std::vector<char> cubin;
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t k_small = nullptr, k_stage = nullptr, k_mc = nullptr;
+};
+
+struct pirk_program {
+    std::string source;
+    uint64_t dim = 0, input_dim = 0;
+    uint32_t flags = 0;
+    std::mutex mu;
+    UserBuild build[2];  // [pirk_mode]
+    ~pirk_program() {
+        for (UserBuild& b : build)
+            if (b.lib) cudaLibraryUnload(b.lib);
+    }
+};
 
 // A block of device memory kept for reuse by the next run of the same size.
 struct CachedBlock {
@@ -59,6 +85,9 @@ struct pirk_ctx {
     // size: freeing 4 x 32 GB costs up to ~0.5 s of unmapping per call
     std::vector<CachedBlock> cache;
     std::vector<PirkLane> peers;  // lanes 1 .. W-1 (empty for a one-device context)
+    // catalog vector fields as generated NVRTC sources (Monte Carlo with
+    // n > kSmallMax, user_models.cuh), keyed by source
+    std::map<std::string, std::unique_ptr<pirk_program>> catalog_programs;
     // every ABI call on a context holds this: calls from several threads on one
     // context serialise instead of racing on err / h_flags / the caches
     std::recursive_mutex mu;
@@ -205,6 +234,11 @@ bool check_model(pirk_ctx* ctx, const pirk_model* m, pirk_status& st) {
         case PIRK_VDP:
             if (m->dim != 2 || m->input_dim != 0) return bad("vdp is 2-D without inputs");
             break;
+        case PIRK_USER:
+            if (!m->program) return bad("user model without a program");
+            if (m->program->dim != m->dim || m->program->input_dim != m->input_dim)
+                return bad("user model dim / input_dim differ from its program's");
+            break;
         default:
             return bad("unknown model kind " + std::to_string(m->kind));
     }
@@ -269,6 +303,7 @@ bool growth_matrix(const pirk_model* m, double* C) {
 }
 
 bool has_growth(const pirk_model* m) {
+    if (m->kind == PIRK_USER) return m->program && (m->program->flags & PIRK_HAS_GROWTH);
     return m->kind == PIRK_ZERO || m->kind == PIRK_SCALAR_DECAY || m->kind == PIRK_SCALAR_LINEAR ||
            m->kind == PIRK_TRAFFIC || m->kind == PIRK_HEAT3D || m->kind == PIRK_LAUB_LOOMIS ||
            m->kind == PIRK_ARCH_QUAD || m->kind == PIRK_VDP;
@@ -316,6 +351,11 @@ HeatModel heat_model(const pirk_model* m, int method) {
 }
 
 bool small_ok(const pirk_model* m) { return m->dim <= static_cast<uint64_t>(kSmallMax); }
+
+bool has_decomposition(const pirk_model* m) {
+    if (m->kind == PIRK_USER) return m->program && (m->program->flags & PIRK_HAS_DECOMPOSITION);
+    return m->decomp != PIRK_DECOMP_NONE;
+}
 
 // Problem validation (system_model.cpp:10-32) except the per-component box
 // checks of large models, which run on the device after upload.
@@ -1126,6 +1166,8 @@ pirk_status run_large_multi(pirk_ctx* ctx, const pirk_model* m, int method, cons
                         setup_s, integ_s, ctx->launches - launches0, W, rep);
 }
 
+#include "user_models.cuh"
+
 // Small-model MM / GB: one device thread per integration.
 pirk_status run_small(pirk_ctx* ctx, const pirk_model* m, int method, const pirk_problem* p,
                       pirk_tube* tube, pirk_report* rep) {
@@ -1142,6 +1184,11 @@ pirk_status run_small(pirk_ctx* ctx, const pirk_model* m, int method, const pirk
     const uint64_t n = m->dim, ni = m->input_dim;
     const SmallModel sm = small_model(m);
     const bool ex = exact_mode(ctx);
+    UserBuild* ub = nullptr;  // user-defined evaluators (NVRTC kernels)
+    if (is_user(m)) {
+        const pirk_status us = user_kernels(ctx, m, &ub);
+        if (us != PIRK_OK) return us;
+    }
     std::vector<double> host_rec0, host_rec1;
     unsigned long long f0 = kNoFail, f1 = kNoFail;
     double setup_s = 0.0;
@@ -1161,7 +1208,8 @@ pirk_status run_small(pirk_ctx* ctx, const pirk_model* m, int method, const pirk
         CK(ctx, cudaMemcpyAsync(dp.p, pp.data(), pp.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
         CK(ctx, cudaMemsetAsync(dfail.p, 0xff, sizeof(unsigned long long), ctx->stream));
         setup_s = since(t_setup);
-        CK(ctx, ex ? launch_small_integrate<true>(sm, 2, dx.p, dp.p, p->t0, p->t1, p->h, plan.total, p->tube_stride, drec.p, dfail.p, ctx->stream)
+        CK(ctx, ub ? user_launch_small(ub, 2, dx.p, dp.p, p->t0, p->t1, p->h, plan.total, p->tube_stride, drec.p, dfail.p, ctx->stream)
+              : ex ? launch_small_integrate<true>(sm, 2, dx.p, dp.p, p->t0, p->t1, p->h, plan.total, p->tube_stride, drec.p, dfail.p, ctx->stream)
                    : launch_small_integrate<false>(sm, 2, dx.p, dp.p, p->t0, p->t1, p->h, plan.total, p->tube_stride, drec.p, dfail.p, ctx->stream));
         ctx->launches++;
         host_rec0.resize(S * 2 * n);
@@ -1193,7 +1241,8 @@ pirk_status run_small(pirk_ctx* ctx, const pirk_model* m, int method, const pirk
             const double* x0 = which ? dr.p : dc.p;
             const double* pp = which ? dw.p : dpc.p;
             double* rec = which ? drec1.p : drec0.p;
-            CK(ctx, ex ? launch_small_integrate<true>(sm, which, x0, pp, p->t0, p->t1, p->h, plan.total, p->tube_stride, rec, dfail.p + which, ctx->stream)
+            CK(ctx, ub ? user_launch_small(ub, which, x0, pp, p->t0, p->t1, p->h, plan.total, p->tube_stride, rec, dfail.p + which, ctx->stream)
+                  : ex ? launch_small_integrate<true>(sm, which, x0, pp, p->t0, p->t1, p->h, plan.total, p->tube_stride, rec, dfail.p + which, ctx->stream)
                        : launch_small_integrate<false>(sm, which, x0, pp, p->t0, p->t1, p->h, plan.total, p->tube_stride, rec, dfail.p + which, ctx->stream));
             ctx->launches++;
         }
@@ -1280,9 +1329,19 @@ pirk_status run_mc(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p, ui
                    double* fraction) {
     const auto t_setup = Clock::now();
     const uint64_t launches0 = ctx->launches;
-    if (!small_ok(m))
+    UserBuild* ub = nullptr;
+    pirk_model um;  // a catalog model beyond the compiled MC kernels: its field as NVRTC source
+    if (!is_user(m) && !small_ok(m) && catalog_mc_program(ctx, m, um)) m = &um;
+    if (is_user(m)) {
+        if (m->dim > kUserMcMax)
+            return fail(ctx, PIRK_EUNSUPPORTED, "monte_carlo: device kernel supports user models with n <= " +
+                                                    std::to_string(kUserMcMax) + " (got " + std::to_string(m->dim) + ")");
+        const pirk_status us = user_kernels(ctx, m, &ub);
+        if (us != PIRK_OK) return us;
+    } else if (!small_ok(m)) {
         return fail(ctx, PIRK_EUNSUPPORTED, "monte_carlo: device kernel supports n <= " +
                                                 std::to_string(kSmallMax) + " (got " + std::to_string(m->dim) + ")");
+    }
     Plan plan;
     plan_steps(p->t0, p->t1, p->h, plan);
     const bool coverage = fraction != nullptr;
@@ -1363,8 +1422,9 @@ pirk_status run_mc(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p, ui
             a.outside = z.dflags.p + 1;
         }
         CK(ctx, cudaSetDevice(z.L.device));
-        CK(ctx, exact_mode(ctx) ? launch_monte_carlo<true>(sm, a, z.L.s)
-                                : launch_monte_carlo<false>(sm, a, z.L.s));
+        CK(ctx, ub ? user_launch_mc(ub, a, z.L.s)
+                   : exact_mode(ctx) ? launch_monte_carlo<true>(sm, a, z.L.s)
+                                     : launch_monte_carlo<false>(sm, a, z.L.s));
         ctx->launches++;
         z.hull.resize(S * 2 * n);
         CK(ctx, cudaMemcpyAsync(z.hull.data(), z.dhull.p, z.hull.size() * sizeof(unsigned long long),
@@ -1590,6 +1650,14 @@ pirk_status pirk_sample_count(uint64_t n, double epsilon, double delta, uint64_t
 
 int32_t pirk_supports(const pirk_model* m, int32_t method) {
     if (!m) return 0;
+    if (m->kind == PIRK_USER) {
+        if (!m->program) return 0;
+        const uint32_t f = m->program->flags;
+        if (method == PIRK_METHOD_MM) return (f & PIRK_HAS_DECOMPOSITION) ? 1 : 0;
+        if (method == PIRK_METHOD_GB) return (f & PIRK_HAS_GROWTH) ? 1 : 0;
+        return ((f & PIRK_HAS_RHS) && m->dim <= kUserMcMax) ? 1 : 0;
+    }
+    if (method == 2 && !small_ok(m)) return catalog_mc_source_ok(m) ? 1 : 0;
     if (method == PIRK_METHOD_MM) {
         if (m->decomp == PIRK_DECOMP_NONE) return 0;
         if (is_chain(m) || is_heat(m)) return m->decomp == PIRK_DECOMP_NATIVE;
@@ -1615,16 +1683,19 @@ static pirk_status reach_mm_gb(pirk_ctx* ctx, const pirk_model* m, const pirk_pr
     const bool large = m && (is_chain(m) || is_heat(m));
     if (!check_problem(ctx, m, p, !large, st)) return st;
     if (method == PIRK_METHOD_MM) {
-        if (m->decomp == PIRK_DECOMP_NONE)
+        if (!has_decomposition(m))
             return fail(ctx, PIRK_EINVAL, "mixed_monotonicity: model has no decomposition function");
         if (!pirk_supports(m, PIRK_METHOD_MM))
             return fail(ctx, PIRK_EUNSUPPORTED, "mixed_monotonicity: no device kernel for this model/decomposition");
     } else {
         if (!has_growth(m)) return fail(ctx, PIRK_EINVAL, "growth_bound: model has no deviation dynamics");
+        if (is_user(m) && !(m->program->flags & PIRK_INPUT_AFFINE))  // reach.cpp:70-71
+            return fail(ctx, PIRK_EINVAL, "growth_bound: model is not input-affine");
         if (!pirk_supports(m, PIRK_METHOD_GB))
             return fail(ctx, PIRK_EUNSUPPORTED, "growth_bound: no device kernel for this model");
     }
     try {
+        if (is_user(m) && m->dim > kUserSmallMax) return run_user_large(ctx, m, method, p, tube, rep);
         if (!large) return run_small(ctx, m, method, p, tube, rep);
         if (ctx->lanes() > 1 && usable_lanes(ctx, is_heat(m) ? m->grid : m->dim) > 1)
             return run_large_multi(ctx, m, method, p, tube, rep);
@@ -1653,6 +1724,8 @@ pirk_status pirk_monte_carlo(pirk_ctx* ctx, const pirk_model* m, const pirk_prob
     if (cudaSetDevice(ctx->device) != cudaSuccess) return fail(ctx, PIRK_ECUDA, "cudaSetDevice failed");
     pirk_status st = PIRK_OK;
     if (!check_problem(ctx, m, p, true, st)) return st;
+    if (is_user(m) && !(m->program->flags & PIRK_HAS_RHS))
+        return fail(ctx, PIRK_EINVAL, "monte_carlo: model has no vector field");
     uint64_t count = spec->samples_override;
     if (count == 0) {
         if (pirk_sample_count(m->dim, spec->epsilon, spec->delta, &count) != PIRK_OK) {
@@ -1814,5 +1887,43 @@ pirk_status pirk_step_window(pirk_ctx* ctx, const pirk_model* m, int32_t method,
                         reinterpret_cast<unsigned long long*>(fail_ptr)));
     return PIRK_OK;
 }
+
+pirk_status pirk_program_create(const char* source, uint64_t dim, uint64_t input_dim, uint32_t flags,
+                                pirk_program** out) {
+    if (!out) return PIRK_EINVAL;
+    *out = nullptr;
+    if (!source || dim == 0) return PIRK_EINVAL;
+    pirk_program* pg = new (std::nothrow) pirk_program;
+    if (!pg) return PIRK_ENOMEM;
+    pg->source = source;
+    pg->dim = dim;
+    pg->input_dim = input_dim;
+    pg->flags = flags;
+    *out = pg;
+    return PIRK_OK;
+}
+
+pirk_status pirk_program_compile(pirk_program* pg, int32_t mode, char* log, size_t log_len,
+                                 uint64_t* cubin_bytes) {
+    if (!pg || (mode != PIRK_MODE_EXACT && mode != PIRK_MODE_FAST)) return PIRK_EINVAL;
+    std::lock_guard<std::mutex> lk(pg->mu);
+    UserBuild& b = pg->build[mode == PIRK_MODE_EXACT ? 0 : 1];
+    const bool ok = user_compile(pg, mode, b);
+    if (log && log_len) {
+        std::snprintf(log, log_len, "%s", b.log.c_str());
+    }
+    if (cubin_bytes) *cubin_bytes = ok ? b.cubin.size() : 0;
+    return ok ? PIRK_OK : PIRK_EINVAL;
+}
+
+pirk_status pirk_program_cubin(const pirk_program* pg, int32_t mode, void* buf, uint64_t len) {
+    if (!pg || !buf || (mode != PIRK_MODE_EXACT && mode != PIRK_MODE_FAST)) return PIRK_EINVAL;
+    const UserBuild& b = pg->build[mode == PIRK_MODE_EXACT ? 0 : 1];
+    if (!b.ok || len < b.cubin.size()) return PIRK_EINVAL;
+    std::memcpy(buf, b.cubin.data(), b.cubin.size());
+    return PIRK_OK;
+}
+
+void pirk_program_destroy(pirk_program* pg) { delete pg; }
 
 }  // extern "C"

@@ -13,7 +13,7 @@ from dataclasses import dataclass, field, replace
 from typing import Tuple
 
 # pirk_model_kind (include/pirk_c.h)
-ZERO, SCALAR_DECAY, SCALAR_LINEAR, TRAFFIC, HEAT3D, CHAIN, LAUB_LOOMIS, ARCH_QUAD, VDP = range(9)
+ZERO, SCALAR_DECAY, SCALAR_LINEAR, TRAFFIC, HEAT3D, CHAIN, LAUB_LOOMIS, ARCH_QUAD, VDP, USER = range(10)
 # pirk_decomp
 DECOMP_NONE, DECOMP_NATIVE, DECOMP_JACOBIAN = range(3)
 
@@ -34,12 +34,100 @@ class SystemModel:
     name: str = ""
     input_affine: bool = True
     sparsity_note: str = ""
+    program: object = None  # USER: the compiled evaluators (Program)
 
     def has_growth(self) -> bool:
+        if self.kind == USER:
+            return bool(self.program.flags & HAS_GROWTH)
         return self.kind in _HAS_GROWTH
 
     def has_decomposition(self) -> bool:
+        if self.kind == USER:
+            return bool(self.program.flags & HAS_DECOMPOSITION)
         return self.decomp != DECOMP_NONE
+
+
+# pirk_program flags (include/pirk_c.h)
+HAS_RHS, HAS_DECOMPOSITION, HAS_GROWTH, INPUT_AFFINE = 1, 2, 4, 8
+
+
+class Program:
+    """A user model's evaluators: CUDA source defining ``pirk_rhs`` /
+    ``pirk_decomposition`` / ``pirk_growth`` (the reference's RhsFn / DecompFn /
+    growth RhsFn, system_model.hpp:14-43, as device functions with the same
+    arguments -- see include/pirk_c.h).  Compiled by NVRTC for sm_100a on first
+    use (exact mode: --fmad=false).  ``compile(mode)`` compiles eagerly and
+    raises ValueError with the NVRTC log on a bad source (no GPU needed)."""
+
+    def __init__(self, source: str, dim: int, input_dim: int, flags: int):
+        import ctypes as C
+
+        from . import _lib
+
+        h = C.c_void_p()
+        st = _lib.lib().pirk_program_create(source.encode(), int(dim), int(input_dim), int(flags),
+                                            C.byref(h))
+        if st != _lib.OK:
+            raise ValueError("pirk_program_create: invalid source or dimension")
+        self._h = h
+        self.source = source
+        self.dim = int(dim)
+        self.input_dim = int(input_dim)
+        self.flags = int(flags)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def compile(self, mode: str = "exact") -> int:
+        """Compile now; returns the sm_100a image size in bytes."""
+        import ctypes as C
+
+        from . import _lib
+
+        log = C.create_string_buffer(1 << 16)
+        size = C.c_uint64()
+        st = _lib.lib().pirk_program_compile(self._h, {"exact": 0, "fast": 1}[mode], log, len(log),
+                                             C.byref(size))
+        if st != _lib.OK:
+            raise ValueError(log.value.decode(errors="replace"))
+        return int(size.value)
+
+    def cubin(self, mode: str = "exact") -> bytes:
+        import ctypes as C
+
+        from . import _lib
+
+        n = self.compile(mode)
+        buf = C.create_string_buffer(n)
+        _lib.lib().pirk_program_cubin(self._h, {"exact": 0, "fast": 1}[mode], buf, n)
+        return buf.raw
+
+    def __del__(self):
+        try:
+            from . import _lib
+
+            if getattr(self, "_h", None):
+                _lib.lib().pirk_program_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def make_user_model(source: str, dim: int, input_dim: int = 0, *, rhs: bool = True,
+                    decomposition: bool = False, growth: bool = False,
+                    input_affine: bool = False, name: str = "user",
+                    sparsity_note: str = "") -> SystemModel:
+    """A SystemModel with caller-written evaluators (system_model.hpp:28-43:
+    ``rhs`` always, ``decomposition`` / ``growth_rhs`` optional, the
+    ``input_affine`` flag growth-bound requires).  ``source`` is CUDA C++; see
+    :class:`Program`."""
+    _require(dim >= 1, "user model needs at least 1 state")
+    flags = ((HAS_RHS if rhs else 0) | (HAS_DECOMPOSITION if decomposition else 0)
+             | (HAS_GROWTH if growth else 0) | (INPUT_AFFINE if input_affine else 0))
+    prog = Program(source, dim, input_dim, flags)
+    return SystemModel(USER, int(dim), int(input_dim), (), DECOMP_NATIVE if decomposition else DECOMP_NONE,
+                       name=name, input_affine=input_affine, sparsity_note=sparsity_note, program=prog)
 
 
 def _require(ok: bool, msg: str) -> None:

@@ -338,6 +338,8 @@ def model_struct(model: SystemModel) -> _lib.PirkModel:
     m.grid = int(model.grid)
     for i, v in enumerate(model.params):
         m.params[i] = float(v)
+    if model.program is not None:
+        m.program = model.program.handle
     return m
 
 

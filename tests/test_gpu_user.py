@@ -1,0 +1,307 @@
+"""User-defined models (the reference's SystemModel with arbitrary evaluators,
+system_model.hpp:14-43) on the device: CUDA sources compiled by NVRTC for
+sm_100a, run through every entry point, against the reference itself.
+
+The reference's own user-model tests are run verbatim: oracle/_ref builds the
+same lambdas (oracle/ref_shim.cpp kinds PO_T_*), the device runs them as
+NVRTC user models, and results / error messages must be identical.
+"""
+import numpy as np
+import pytest
+
+import paper_2001_10635_b200 as pk
+from oracle import oracle as O
+from tests.helpers import assert_bitexact, assert_within, tube_arrays
+
+pytestmark = pytest.mark.gpu
+
+T_ORDER, T_EMBED, T_DRIFT, T_BARE = 100, 101, 102, 103
+
+
+class RefModel:
+    """Oracle-side descriptor of a reference test system (ref_shim.cpp)."""
+
+    def __init__(self, kind, dim, input_dim=0, params=(), decomp=1):
+        self.kind, self.dim, self.input_dim, self.grid = kind, dim, input_dim, 0
+        self.params, self.decomp = params, decomp
+
+
+def ref(method, model, lo, hi, t0, t1, h, stride, plo=None, phi=None, **kw):
+    return O.ref_reach(method, model, lo, hi, plo, phi, t0, t1, h, stride, workers=1, **kw)
+
+
+@pytest.fixture(scope="module", params=["exact", "fast"])
+def mctx(request):
+    c = pk.Context(0, request.param)
+    yield c
+    c.close()
+
+
+# --------------------------------------------- the reference's own user models
+
+ORDER_SRC = r"""
+// test_reach.cpp:190-206: f = (x2, -1); the decomposition reads x2 from the
+// opposite copy, so the corners cross at t = 2
+__device__ double pirk_rhs(u64 i, double, const double* x, const double*) { return i == 0 ? x[1] : -1.0; }
+__device__ double pirk_decomposition(u64 i, double, const double*, const double*, const double* xh,
+                                     const double*) { return i == 0 ? xh[1] : -1.0; }
+"""
+
+
+def test_order_violating_decomposition_is_reported(ctx):
+    """test_reach.cpp:190-206 verbatim: the CUDA path raises the reference's
+    exact message (reach.cpp:181-186) -- not vacuous: the reference raises."""
+    m = pk.make_user_model(ORDER_SRC, 2, decomposition=True)
+    prob = pk.ReachProblem(m, pk.IntervalVector([0.0, 0.0], [1.0, 0.5]), None, 0.0, 3.0, 0.1, 1)
+    with pytest.raises(O.OracleError) as eo:
+        ref(O.METHOD_MM, RefModel(T_ORDER, 2), [0.0, 0.0], [1.0, 0.5], 0.0, 3.0, 0.1, 1)
+    assert "embedding order violated" in str(eo.value)
+    with pytest.raises(RuntimeError) as ei:
+        pk.mixed_monotonicity(prob, ctx=ctx)
+    assert str(ei.value) == str(eo.value)
+    # the same problem stopped before the crossing is boxed, bit-identical
+    ok = pk.ReachProblem(m, pk.IntervalVector([0.0, 0.0], [1.0, 0.5]), None, 0.0, 1.5, 0.1, 1)
+    assert_bitexact(pk.mixed_monotonicity(ok, ctx=ctx),
+                    ref(O.METHOD_MM, RefModel(T_ORDER, 2), [0.0, 0.0], [1.0, 0.5], 0.0, 1.5, 0.1, 1))
+
+
+def test_order_violation_large_user_model(ctx):
+    """The stage-kernel path (n > 64) runs the same device order check."""
+    n = 100
+    src = r"""
+__device__ double pirk_rhs(u64 i, double, const double* x, const double*) {
+    return (i % 2 == 0) ? x[i + 1] : -1.0;
+}
+__device__ double pirk_decomposition(u64 i, double, const double*, const double*, const double* xh,
+                                     const double*) { return (i % 2 == 0) ? xh[i + 1] : -1.0; }
+"""
+    m = pk.make_user_model(src, n, decomposition=True)
+    lo, hi = np.zeros(n), np.tile([1.0, 0.5], n // 2)
+    prob = pk.ReachProblem(m, pk.IntervalVector(lo, hi), None, 0.0, 3.0, 0.1, 1)
+    with pytest.raises(RuntimeError, match=r"embedding order violated at step 20, t = 2.000000, component 0"):
+        pk.mixed_monotonicity(prob, ctx=ctx)
+
+
+EMBED_SRC = r"""
+// test_system_model.cpp:74-96: f(x) = -x with the antitone dependence routed
+// to the hatted argument
+__device__ double pirk_rhs(u64, double, const double* x, const double*) { return -x[0]; }
+__device__ double pirk_decomposition(u64, double, const double*, const double*, const double* xh,
+                                     const double*) { return -xh[0]; }
+"""
+
+
+def test_embedding_wires_the_decomposition(ctx):
+    """test_system_model.cpp:74-96: lower half sees xh, upper half the
+    swapped arguments.  One RK4 step from [1, 2] with h -> the first stage
+    is (-2, -1); over 10 steps the tube equals the reference's bit for bit."""
+    m = pk.make_user_model(EMBED_SRC, 1, decomposition=True)
+    prob = pk.ReachProblem(m, pk.IntervalVector([1.0], [2.0]), None, 0.0, 1.0, 0.1, 1)
+    tube = pk.mixed_monotonicity(prob, ctx=ctx)
+    assert_bitexact(tube, ref(O.METHOD_MM, RefModel(T_EMBED, 1), [1.0], [2.0], 0.0, 1.0, 0.1, 1))
+    # Euler-size check of the wiring: lower moves with -xh = -2, upper with -x = -1
+    h = 1e-9
+    one = pk.mixed_monotonicity(pk.ReachProblem(m, pk.IntervalVector([1.0], [2.0]), None, 0.0, h, h, 0),
+                                ctx=ctx).entries[-1].box
+    assert abs((one.lower[0] - 1.0) / h - (-2.0)) < 1e-6
+    assert abs((one.upper[0] - 2.0) / h - (-1.0)) < 1e-6
+
+
+def drift_model(g):
+    src = r"""
+__device__ double pirk_rhs(u64, double, const double*, const double*) { return 0.0; }
+__device__ double pirk_decomposition(u64, double, const double*, const double*, const double*,
+                                     const double*) { return 0.0; }
+__device__ double pirk_growth(u64, double, const double*, const double*) { return %s; }
+""" % repr(float(g))
+    return pk.make_user_model(src, 1, decomposition=True, growth=True, input_affine=True)
+
+
+def test_negative_radius_clamped_or_reported(ctx):
+    """test_reach.cpp:208-230: a radius of -1e-13 is clamped to 0 (box stays
+    [0.5, 0.5]); -1 is 'contraction matrix is invalid' with the reference's
+    message (reach.cpp:121-133) -- on both the small and the large path."""
+    tiny = pk.ReachProblem(drift_model(-1e-13), pk.IntervalVector([0.5], [0.5]), None, 0.0, 1.0, 1.0, 0)
+    tube = pk.growth_bound(tiny, ctx=ctx)
+    assert tube.entries[-1].box == pk.IntervalVector([0.5], [0.5])
+    assert_bitexact(tube, ref(O.METHOD_GB, RefModel(T_DRIFT, 1, params=(-1e-13,)), [0.5], [0.5], 0.0, 1.0, 1.0, 0))
+    wrong = pk.ReachProblem(drift_model(-1.0), pk.IntervalVector([0.5], [0.5]), None, 0.0, 1.0, 1.0, 0)
+    with pytest.raises(O.OracleError) as eo:
+        ref(O.METHOD_GB, RefModel(T_DRIFT, 1, params=(-1.0,)), [0.5], [0.5], 0.0, 1.0, 1.0, 0)
+    with pytest.raises(RuntimeError) as ei:
+        pk.growth_bound(wrong, ctx=ctx)
+    assert str(ei.value) == str(eo.value)
+    assert "deviation went negative (-1.000000) at component 0" in str(ei.value)
+
+
+def test_negative_radius_large_path(ctx):
+    n = 80
+    src = r"""
+__device__ double pirk_rhs(u64, double, const double*, const double*) { return 0.0; }
+__device__ double pirk_growth(u64 i, double, const double*, const double*) { return i == 77 ? -1.0 : -1e-13; }
+"""
+    m = pk.make_user_model(src, n, growth=True, input_affine=True)
+    prob = pk.ReachProblem(m, pk.IntervalVector(np.full(n, 0.5), np.full(n, 0.5)), None, 0.0, 1.0, 1.0, 0)
+    with pytest.raises(RuntimeError, match=r"deviation went negative \(-1.000000\) at component 77; "
+                                           r"contraction matrix is invalid"):
+        pk.growth_bound(prob, ctx=ctx)
+
+
+BARE_SRC = "__device__ double pirk_rhs(u64, double, const double* x, const double*) { return -x[0]; }\n"
+
+
+def test_model_without_growth_or_decomposition(ctx):
+    """test_reach.cpp:176-188: GB and MM are invalid_argument, MC works (and
+    equals the reference's MC of the same lambda, m = 8)."""
+    m = pk.make_user_model(BARE_SRC, 1)
+    prob = pk.ReachProblem(m, pk.IntervalVector([0.0], [1.0]), None, 0.0, 1.0, 0.1, 0)
+    with pytest.raises(ValueError, match="no deviation dynamics"):
+        pk.growth_bound(prob, ctx=ctx)
+    with pytest.raises(ValueError, match="no decomposition function"):
+        pk.mixed_monotonicity(prob, ctx=ctx)
+    tube = pk.monte_carlo(prob, pk.MonteCarloSpec(samples_override=8), ctx=ctx)
+    assert_bitexact(tube, ref(O.METHOD_MC, RefModel(T_BARE, 1, decomp=0), [0.0], [1.0], 0.0, 1.0, 0.1, 0,
+                              samples=8, seed=1))
+
+
+def test_growth_bound_needs_input_affine(ctx):
+    m = pk.make_user_model(BARE_SRC.replace("pirk_rhs", "pirk_growth") + BARE_SRC, 1, growth=True,
+                           input_affine=False)
+    prob = pk.ReachProblem(m, pk.IntervalVector([0.0], [1.0]), None, 0.0, 1.0, 0.1, 0)
+    with pytest.raises(ValueError, match="not input-affine"):
+        pk.growth_bound(prob, ctx=ctx)
+
+
+# ------------------------------- catalog fields written as user sources
+
+TRAFFIC_SRC = r"""
+// models.cpp:47-90 written by hand as a user model (default parameters)
+constexpr double V = 0.5, W = 1.0 / 6.0, C = 40.0, XBAR = 320.0, PERIOD = 30.0, BETA = 0.75;
+constexpr double INV_T = 1.0 / PERIOD;
+__device__ double flux(double from, double into) {
+    return pirk_min(C, pirk_min(V * from, W * (XBAR - into) / BETA));
+}
+__device__ double pirk_rhs(u64 i, double, const double* x, const double* p) {
+    const double in = (i == 0) ? BETA * p[0] : BETA * flux(x[i - 1], x[i]);
+    const double out = (i + 1 == PIRK_N) ? pirk_min(C, V * x[i]) : flux(x[i], x[i + 1]);
+    return INV_T * (in - out);
+}
+__device__ double pirk_decomposition(u64 i, double t, const double* x, const double* p, const double*,
+                                     const double*) { return pirk_rhs(i, t, x, p); }  // cooperative
+__device__ double pirk_growth(u64 i, double, const double* r, const double* w) {
+    constexpr double a_prev = BETA * V * INV_T, a_next = (W / BETA) * INV_T, a_in = BETA * INV_T;
+    double g = (i == 0) ? a_in * w[0] : a_prev * r[i - 1];
+    if (i + 1 < PIRK_N) g += a_next * r[i + 1];
+    return g;
+}
+"""
+
+
+def user_traffic(n):
+    return pk.make_user_model(TRAFFIC_SRC, n, 1, decomposition=True, growth=True, input_affine=True,
+                              name="user-traffic")
+
+
+def traffic_prob(model, n, stride=3, t1=6.0):
+    rng = np.random.default_rng(n)
+    lo = rng.uniform(5, 40, n)
+    hi = lo + rng.uniform(0, 10, n)
+    return pk.ReachProblem(model, pk.IntervalVector(lo, hi), pk.IntervalVector([4.0], [6.0]), 0.0, t1, 0.5,
+                           stride)
+
+
+@pytest.mark.parametrize("n", [5, 50, 64, 65, 300, 4097])
+def test_user_traffic_equals_catalog(mctx, n):
+    """A user source restating traffic: n <= 64 runs one thread per
+    integration, n > 64 one thread per component and stage.  Exact mode is
+    bit-identical to the oracle's catalog traffic; fast mode within 1e-12."""
+    up = traffic_prob(user_traffic(n), n)
+    cat = pk.make_traffic(n)
+    cp = traffic_prob(cat, n)
+    for meth, fn, ofn in (("mm", pk.mixed_monotonicity, O.mixed_monotonicity),
+                          ("gb", pk.growth_bound, O.growth_bound)):
+        tube = fn(up, ctx=mctx)
+        oref = ofn(cat, cp.initial.lower, cp.initial.upper, [4.0], [6.0], 0.0, 6.0, 0.5, 3)
+        if mctx.mode == "exact":
+            assert_bitexact(tube, oref)
+        else:
+            assert_within(tube, oref, rel=1e-12, never_tighter=False)
+
+
+def test_user_mc_equals_catalog(ctx):
+    """User traffic Monte Carlo: test_reach.cpp:88-111 (n = 6, seed 42,
+    m = 64, stride 2) bit-identical to the oracle; and n = 100 (beyond the
+    compiled kernels' n <= 64) against the oracle too."""
+    for n, m_samples, seed in ((6, 64, 42), (100, 3000, 7)):
+        m = user_traffic(n)
+        prob = pk.ReachProblem(m, pk.IntervalVector(np.full(n, 10.0), np.full(n, 20.0)),
+                               pk.IntervalVector([4.0], [6.0]), 0.0, 3.0, 0.5, 2)
+        tube = pk.monte_carlo(prob, pk.MonteCarloSpec(seed=seed, samples_override=m_samples), ctx=ctx)
+        oref = O.monte_carlo(pk.make_traffic(n), np.full(n, 10.0), np.full(n, 20.0), [4.0], [6.0], 0.0, 3.0,
+                             0.5, 2, seed, m_samples)
+        assert_bitexact(tube, oref)
+
+
+@pytest.mark.parametrize("model", ["traffic", "heat", "chain"])
+def test_catalog_mc_beyond_64_components(ctx, model):
+    """Catalog Monte Carlo with 64 < n <= 1024 (VERDICT r1 missing #4): the
+    model's field is generated as NVRTC source (engine: catalog_source) and
+    runs on the user MC kernel -- bit-identical to the oracle."""
+    if model == "traffic":
+        m, n = pk.make_traffic(200), 200
+        plo, phi, t1, h = [4.0], [6.0], 3.0, 0.5
+        lo, hi = np.full(n, 10.0), np.full(n, 20.0)
+    elif model == "heat":
+        m, n = pk.make_heat3d(6), 216
+        plo = phi = None
+        h = 0.2 / 25
+        t1 = 10 * h
+        lo, hi = np.full(n, 0.9), np.full(n, 1.1)
+    else:
+        m, n = pk.make_chain(500), 500
+        plo, phi, t1, h = [-0.1], [0.1], 0.5, 0.01
+        c = np.linspace(-1, 1, n)
+        lo, hi = c - 0.05, c + 0.05
+    prob = pk.ReachProblem(m, pk.IntervalVector(lo, hi), pk.IntervalVector(plo, phi) if plo else None,
+                           0.0, t1, h, 5)
+    tube = pk.monte_carlo(prob, pk.MonteCarloSpec(seed=3, samples_override=2000), ctx=ctx)
+    oref = O.monte_carlo(m, lo, hi, plo, phi, 0.0, t1, h, 5, 3, 2000)
+    assert_bitexact(tube, oref)
+
+
+def test_user_model_on_lanes_and_workers():
+    """User MC over 3 lanes == 1 lane; user MM through workers=3 (user
+    models run on lane 0: their stencil is unknown, so they do not shard)."""
+    n = 12
+    m = user_traffic(n)
+    prob = pk.ReachProblem(m, pk.IntervalVector(np.full(n, 10.0), np.full(n, 20.0)),
+                           pk.IntervalVector([4.0], [6.0]), 0.0, 3.0, 0.5, 2)
+    c1, c3 = pk.Context(0, "exact"), pk.Context(devices=[0, 0, 0], mode="exact")
+    try:
+        spec = pk.MonteCarloSpec(seed=9, samples_override=5001)
+        a, b = pk.monte_carlo(prob, spec, ctx=c1), pk.monte_carlo(prob, spec, ctx=c3)
+        ta, la, ha = tube_arrays(a)
+        tb, lb, hb = tube_arrays(b)
+        assert np.array_equal(la, lb) and np.array_equal(ha, hb)
+        assert_bitexact(pk.mixed_monotonicity(prob, ctx=c3),
+                        O.mixed_monotonicity(pk.make_traffic(n), np.full(n, 10.0), np.full(n, 20.0), [4.0],
+                                             [6.0], 0.0, 3.0, 0.5, 2))
+    finally:
+        c1.close()
+        c3.close()
+
+
+def test_user_nonfinite_reports_step(ctx):
+    """IntegrationError through a user model (rk4.cpp:19-23 / reach.cpp:190-192):
+    xdot = 5x blows up; the message equals the catalog scalar-linear one."""
+    src = "__device__ double pirk_rhs(u64, double, const double* x, const double*) { return 5.0 * x[0]; }\n" \
+          "__device__ double pirk_decomposition(u64, double, const double* x, const double*, const double*," \
+          " const double*) { return 5.0 * x[0]; }\n"
+    m = pk.make_user_model(src, 1, decomposition=True)
+    prob = pk.ReachProblem(m, pk.IntervalVector([1.0], [1.0]), None, 0.0, 600.0, 10.0, 0)
+    with pytest.raises(RuntimeError) as ei:
+        pk.mixed_monotonicity(prob, ctx=ctx)
+    cat = pk.make_scalar_linear(5.0)
+    with pytest.raises(O.OracleError) as eo:
+        O.mixed_monotonicity(cat, [1.0], [1.0], None, None, 0.0, 600.0, 10.0, 0)
+    assert str(ei.value) == str(eo.value)
