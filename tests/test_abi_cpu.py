@@ -85,7 +85,9 @@ def test_capability_table():
     assert not sup(pk.make_arch_quadrotor(), 0)
     assert sup(pk.with_jacobian_decomposition(pk.make_arch_quadrotor()), 0)
     assert sup(pk.make_arch_quadrotor(), 1) and sup(pk.make_arch_quadrotor(), 2)
-    assert not sup(pk.make_traffic(100), 2)  # MC kernel is for n <= 64
+    # MC: compiled kernels for n <= 64, generated-source (NVRTC) kernel for n <= 1024
+    assert sup(pk.make_traffic(100), 2) and sup(pk.make_heat3d(10), 2)
+    assert not sup(pk.make_traffic(2000), 2) and not sup(pk.make_heat3d(11), 2)
 
 
 def test_interval_and_problem_validation_messages():

@@ -362,8 +362,8 @@ def test_order_violation_reported(ctx):
 
 
 def test_unsupported_model_is_loud(ctx):
-    m = pk.make_traffic(100)  # Monte Carlo kernel is for n <= 64
-    prob = pk.ReachProblem(m, pk.IntervalVector(np.zeros(100), np.ones(100)),
+    m = pk.make_traffic(2000)  # Monte Carlo kernels hold a sample in registers: n <= 1024
+    prob = pk.ReachProblem(m, pk.IntervalVector(np.zeros(2000), np.ones(2000)),
                            pk.IntervalVector([1.0], [2.0]), 0.0, 1.0, 0.5, 0)
     with pytest.raises(NotImplementedError):
         pk.monte_carlo(prob, pk.MonteCarloSpec(samples_override=10), ctx=ctx)
