@@ -337,39 +337,91 @@ def heat_e2e_sharded(args, pk, torch, dist, world, rank, local):
     return res
 
 
+def fp64_peak():
+    """Measured FP64 pipe peak (profiles/r02_fp64_peak.json, DFMA/DADD/DMUL
+    microbenchmark on this pool's B200): instructions/s (the largest of the
+    three, so fractions are conservative) and TFLOP/s (DFMA = 2 flops)."""
+    with open(os.path.join(ROOT, "profiles", "r02_fp64_peak.json")) as f:
+        p = json.load(f)
+    return max(p["dfma_per_s"], p["dadd_per_s"], p["dmul_per_s"]), p["fp64_tflops_fma"]
+
+
+def fp64_counts():
+    """Executed FP64 instructions / flops per unit of work of each secondary
+    kernel (ncu SASS counters, profiles/r02_fp64_counts.json)."""
+    with open(os.path.join(ROOT, "profiles", "r02_fp64_counts.json")) as f:
+        return json.load(f)["kernels"]
+
+
+def fp64_roofline(rate, key, kernel):
+    inst_peak, tflops_peak = fp64_peak()
+    c = fp64_counts()[key]
+    inst = c["fp64_inst_per_unit"] * rate
+    flops = c["fp64_flops_per_unit"] * rate
+    return {"bound": "fp64", "achieved": inst / 1e12, "peak": inst_peak / 1e12,
+            "unit": "T FP64 inst/s", "frac": inst / inst_peak,
+            "achieved_tflops": flops / 1e12, "peak_tflops": tflops_peak,
+            "frac_flops": flops / 1e12 / tflops_peak, "kernel": kernel,
+            "fp64_inst_per_unit": c["fp64_inst_per_unit"], "fp64_flops_per_unit": c["fp64_flops_per_unit"],
+            "ncu_pipe_fp64_pct": c["pipe_fp64_pct"],
+            "counts_from": "profiles/r02_fp64_counts.json (ncu SASS counters); peak: profiles/r02_fp64_peak.json"}
+
+
+def host_ram_gb():
+    import psutil
+
+    vm = psutil.virtual_memory()
+    return vm.total / 2 ** 30, vm.available / 2 ** 30
+
+
 def cpu_baseline(args):
-    """The reference itself (oracle/_ref) on this host, bounded sample."""
+    """The reference itself (oracle/_ref) on this host, bounded sample at the
+    largest heat3d grid the host RAM holds (the reference keeps 7 vectors of
+    2n doubles, 112n bytes, plus the 4n-double box arrays here), capped so the
+    sample is ~20 s of CPU work (C5's g = 1600 needs 459 GB)."""
     from oracle import oracle as O
 
     import paper_2001_10635_b200 as pk
 
     if not O.ref_available():
         return None
-    g, steps = args.cpu_grid, args.cpu_steps
+    total_gb, avail_gb = host_ram_gb()
+    g_ram = int((0.8 * avail_gb * 2 ** 30 / 150.0) ** (1.0 / 3.0))
+    g = max(args.cpu_grid, min(g_ram, args.cpu_grid_max))
+    steps = args.cpu_steps
     model = pk.make_heat3d(g)
     n = g ** 3
     threads = O.ref_max_threads()
     r = O.ref_reach(O.METHOD_MM, model, np.full(n, 0.9), np.full(n, 1.1), None, None, 0.0,
                     steps * args.h, args.h, 0, workers=threads, keep=False)
     rate = 2.0 * n * steps / r.report["integration_s"]
-    # the same reference on one worker (SURVEY.md 8d: all cores and 1), over a
-    # quarter of the sample's steps to stay within the bench's time budget
-    s1 = max(1, steps // 4)
-    r1 = O.ref_reach(O.METHOD_MM, model, np.full(n, 0.9), np.full(n, 1.1), None, None, 0.0,
-                     s1 * args.h, args.h, 0, workers=1, keep=False)
+    # the same reference on one worker (SURVEY.md 8d: all cores and 1), on a
+    # small grid to stay within the bench's time budget
+    g1, s1 = 300, 2
+    n1 = g1 ** 3
+    r1 = O.ref_reach(O.METHOD_MM, pk.make_heat3d(g1), np.full(n1, 0.9), np.full(n1, 1.1), None, None,
+                     0.0, s1 * args.h, args.h, 0, workers=1, keep=False)
     return {"value": rate, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"ivreach::mixed_monotonicity (oracle/_ref, -O3, OpenMP) heat3d grid={g} "
-                      f"(n={n}), {steps} RK4 steps, h={args.h}; rate = 2n*steps/integration_s",
-            "wall_s": r.wall_s,
-            "single_worker": {"value": 2.0 * n * s1 / r1.report["integration_s"], "cores": 1,
-                              "steps": s1}}
+            "sample": f"ivreach::mixed_monotonicity (oracle/_ref, -O3, OpenMP, x86-64 baseline, no FMA) "
+                      f"heat3d grid={g} (n={n}), {steps} RK4 steps, h={args.h}; rate = 2n*steps/integration_s; "
+                      f"grid = the largest the host RAM holds (capped at {args.cpu_grid_max})",
+            "host_ram_gb": round(total_gb, 1), "host_ram_available_gb": round(avail_gb, 1),
+            "reference_state_gb": round(112.0 * n / 1e9, 1),
+            "wall_s": r.wall_s, "integration_s": r.report["integration_s"],
+            "single_worker": {"value": 2.0 * n1 * s1 / r1.report["integration_s"], "cores": 1,
+                              "grid": g1, "steps": s1}}
 
 
 def secondary(args, pk, torch):
-    """Other BASELINE configs on one GPU (quick lines, not the headline)."""
+    """The other BASELINE configs on one GPU, each with the roofline that
+    bounds it and the reference timed beside it on the host cores."""
+    from oracle import oracle as O
+
     out = {}
     ctx = pk.get_context(0)
     ctx.set_mode(args.mode)
+    ref_ok = O.ref_available() and not args.no_cpu
+    threads = O.ref_max_threads() if ref_ok else 0
 
     def engine_rate(prob, steps=20):
         eng = pk.Engine(prob, ctx=ctx)
@@ -388,27 +440,51 @@ def secondary(args, pk, torch):
         ctx.set_stream(None)
         return 2.0 * prob.model.dim / (ms * 1e-3), ms
 
-    # C3: traffic n=1e6 CTMM
+    def ref_rate(method, prob, **kw):
+        p = prob
+        plo = p.inputs.lower if p.inputs is not None else None
+        phi = p.inputs.upper if p.inputs is not None else None
+        r = O.ref_reach(method, p.model, p.initial.lower, p.initial.upper, plo, phi, p.t0, p.t1, p.h,
+                        p.tube_stride, workers=threads, keep=False, **kw)
+        return r
+
+    hbm, _ = peaks()
+    # C3: traffic n = 1e6 CTMM.  The 4 state buffers (32 MB) stay in the 126 MB
+    # L2 and a step is ~10 us: launch / latency and the FP64 pipe bound it, not
+    # HBM (the HBM fraction is kept for comparison only).
     n = 10 ** 6
     m = pk.make_traffic(n)
     p = pk.ReachProblem(m, pk.IntervalVector(np.full(n, 10.0), np.full(n, 20.0)),
                         pk.IntervalVector([4.0], [6.0]), 0.0, 30.0, 0.5, 0)
     v, ms = engine_rate(p, 40)
-    hbm, _ = peaks()
-    # K1 roofline: 16 B of HBM per state-update; C3's 32 MB state is
-    # L2-resident, so its fraction understates what bounds it
-    out["C3_traffic_ctmm_n1e6"] = {"value": v, "unit": UNIT, "ms_per_step": ms,
-                                   "hbm_roofline_frac": v * 16.0 / (hbm * 1e9), "kernel": "chain_warp_kernel"}
-    # C4: coupled chain n=1e7 (SDMM interpretation)
+    c3 = {"value": v, "unit": UNIT, "ms_per_step": ms, "kernel": "chain_warp_kernel",
+          "roofline": fp64_roofline(v, f"traffic_{args.mode}", "chain_warp_kernel"),
+          "hbm_frac_if_streamed": v * 16.0 / (hbm * 1e9),
+          "note": "state (4 x 8 MB) is L2-resident; ~10 us per RK4 step"}
+    if ref_ok:
+        r = ref_rate(O.METHOD_MM, p)
+        c3["cpu_baseline"] = {"value": 2.0 * n * r.report["steps"] / r.report["integration_s"], "unit": UNIT,
+                              "cores": threads, "kind": "reference",
+                              "sample": "ivreach::mixed_monotonicity traffic n=1e6, 60 steps (the full C3 reach)"}
+    out["C3_traffic_ctmm_n1e6"] = c3
+    # C4: coupled chain n = 1e7 (SDMM interpretation): FP64-bound
     n = 10 ** 7
     m = pk.make_chain(n)
-    c = 2.0 * np.random.default_rng(7).random(n) - 1.0
-    p = pk.ReachProblem(m, pk.IntervalVector(c - 0.05, c + 0.05), pk.IntervalVector([-0.1], [0.1]),
+    ctr = 2.0 * O.u01_vec(7, 0, np.arange(n, dtype=np.uint64)) - 1.0
+    p = pk.ReachProblem(m, pk.IntervalVector(ctr - 0.05, ctr + 0.05), pk.IntervalVector([-0.1], [0.1]),
                         0.0, 1.0, 0.01, 0)
     v, ms = engine_rate(p, 40)
-    out["C4_chain_sdmm_n1e7"] = {"value": v, "unit": UNIT, "ms_per_step": ms,
-                                 "hbm_roofline_frac": v * 16.0 / (hbm * 1e9), "kernel": "chain_warp_kernel"}
-    # C2: arch-quadrotor Monte Carlo, m = 1e6, 100 steps
+    c4 = {"value": v, "unit": UNIT, "ms_per_step": ms, "kernel": "chain_warp_kernel",
+          "roofline": fp64_roofline(v, f"chain_{args.mode}", "chain_warp_kernel"),
+          "hbm_frac": v * 16.0 / (hbm * 1e9)}
+    if ref_ok:
+        p10 = pk.ReachProblem(m, p.initial, p.inputs, 0.0, 0.1, 0.01, 0)
+        r = ref_rate(O.METHOD_MM, p10)
+        c4["cpu_baseline"] = {"value": 2.0 * n * r.report["steps"] / r.report["integration_s"], "unit": UNIT,
+                              "cores": threads, "kind": "reference",
+                              "sample": "ivreach::mixed_monotonicity chain n=1e7, first 10 of the 100 steps"}
+    out["C4_chain_sdmm_n1e7"] = c4
+    # C2: arch-quadrotor Monte Carlo, m = 1e6, 100 steps: FP64-bound
     mq = pk.make_arch_quadrotor()
     lo = np.array([-0.4] * 6 + [0.0] * 6)
     p = pk.ReachProblem(mq, pk.IntervalVector(lo, -lo), None, 0.0, 1.0, 0.01, 0)
@@ -417,10 +493,65 @@ def secondary(args, pk, torch):
     t0 = time.perf_counter()
     tube = pk.monte_carlo(p, spec, ctx=ctx)
     dt = time.perf_counter() - t0
-    out["C2_archquad_mc_m1e6"] = {"value": 1e6 * tube.report.steps / dt, "unit": "sample-steps/s",
-                                  "kernel_s": tube.report.phases.integration_s,
-                                  "kernel_value": 1e6 * tube.report.steps / tube.report.phases.integration_s}
+    kv = 1e6 * tube.report.steps / tube.report.phases.integration_s
+    c2 = {"value": 1e6 * tube.report.steps / dt, "unit": "sample-steps/s",
+          "kernel_s": tube.report.phases.integration_s, "kernel_value": kv,
+          "roofline": fp64_roofline(kv, f"mc_{args.mode}", "monte_carlo_kernel")}
+    if ref_ok:
+        ms_ = 10 ** 5
+        r = ref_rate(O.METHOD_MC, p, samples=ms_, seed=1)
+        c2["cpu_baseline"] = {"value": ms_ * r.report["steps"] / r.report["integration_s"],
+                              "unit": "sample-steps/s", "cores": threads, "kind": "reference",
+                              "sample": f"ivreach::monte_carlo arch-quadrotor m={ms_} (of 1e6), 100 steps"}
+    out["C2_archquad_mc_m1e6"] = c2
     return out
+
+
+def sharded_chain_bench(args, world, rank, local, torch, pk, dist):
+    """BASELINE config 4 at N GPUs: the coupled chain n = 1e7 sharded into
+    index ranges with deep halos (K = 8 steps per exchange, 32-unit halos: the
+    1-D halo is pure latency), NCCL point-to-point between ranks; 100-step
+    reach timed on the device, max over ranks."""
+    from paper_2001_10635_b200 import sharded as S
+
+    n, K, steps = 10 ** 7, 8, 100
+    model = pk.make_chain(n)
+    ctx = pk.Context(local, args.mode)
+    shard = S.Shard(n, world, rank, 4 * K)
+    run = S.ShardedReach(model, "mixed-monotonicity", shard, S.device_step_fn(model, "mixed-monotonicity", ctx),
+                         S.HaloExchanger(shard, 1) if world > 1 else None, [-0.1], [0.1], K=K)
+    dev = torch.device("cuda", local)
+    fail = torch.full((2,), -1, dtype=torch.int64, device=dev)
+    a = run.alloc(lambda k: torch.empty(k, dtype=torch.float64, device=dev), fail=fail)
+    idx = torch.arange(shard.win_begin, shard.win_end, dtype=torch.float64, device=dev)
+    a[0].copy_(torch.sin(idx) - 0.05)
+    a[1].copy_(torch.sin(idx) + 0.05)
+    plan = S.plan_rk4_steps(0.0, steps * 0.01, 0.01)
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        run.run(plan[:K], 0)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        run.run(plan[K:], K)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    run.check(0.0, 0.01)
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    del a, run
+    torch.cuda.empty_cache()
+    ctx.close()
+    timed = steps - K
+    return {"value": 2.0 * n * timed / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / timed,
+            "n_gpus": world, "halo_units": 4 * K, "steps_per_exchange": K,
+            "workload": "C4 coupled chain n=1e7 CTMM, index-range shards, NCCL halos, 92 timed steps",
+            "scaling": "strong"}
 
 
 def run_ours(args):
@@ -497,6 +628,10 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_baseline(args)
     if rank == 0 and world == 1 and not args.no_secondary:
         line["secondary"] = secondary(args, pk, torch)
+    if not args.no_secondary:  # config 4 at N GPUs (the N = 1 value is its baseline)
+        c4n = sharded_chain_bench(args, world, rank, local, torch, pk, dist)
+        if rank == 0:
+            line.setdefault("secondary", {})["C4_chain_sharded_nGPU"] = c4n
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -568,7 +703,8 @@ def main():
     ap.add_argument("--grid", type=int, default=GRID)
     ap.add_argument("--h", type=float, default=H)
     ap.add_argument("--cpu-grid", type=int, default=300)
-    ap.add_argument("--cpu-steps", type=int, default=10)
+    ap.add_argument("--cpu-grid-max", type=int, default=1000)
+    ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--ref-steps-per-call", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -14,6 +14,10 @@
 //   u3 = x + hk*k2; k3 = f(u3); x' = x + h6*(((k0 + 2k1) + 2k2) + k3).
 #pragma once
 
+#ifndef PIRK_DEV_VARIANTS
+#define PIRK_DEV_VARIANTS 0  // 1: also build the rejected smem-tile chain kernel
+#endif
+
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -63,6 +67,7 @@ __device__ __forceinline__ double chain_sat(double z) {
     }
 }
 
+#if PIRK_DEV_VARIANTS  // the rejected shared-memory tile kernel (A/B and reference only)
 template <bool Exact, int Kind, int Method>
 __global__ void __launch_bounds__(kChainThreads)
 chain_step_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc,
@@ -224,6 +229,7 @@ chain_step_kernel(const ChainModel m, const WindowArgs w, const StepConsts sc,
         }
     }
 }
+#endif  // PIRK_DEV_VARIANTS
 
 // ---------------------------------------------------------------------------
 // Warp-tiled variant (the default): each warp owns a segment of 32 * kCwP
@@ -487,15 +493,20 @@ cudaError_t launch_chain_step(const ChainModel& m, const WindowArgs& w, const St
     // tiles: fast traffic 0.097 vs 0.139, chain 0.0995 vs 0.135; exact traffic
     // 0.165 vs 0.202, chain 0.153 vs 0.163).  PIRK_CHAIN_KERNEL=smem|warp
     // overrides (A/B comparisons, parity tests of both kernels).
+#if PIRK_DEV_VARIANTS
     static const bool use_smem = [] {
         const char* v = std::getenv("PIRK_CHAIN_KERNEL");
         return v && std::strcmp(v, "smem") == 0;
     }();
+#else
+    const bool use_smem = false;
+#endif
     if (!use_smem) {
         StepConstsN one;
         one.s[0] = sc;
         return launch_chain_warp<Exact, 1>(m, w, one, step, fail, stream);
     }
+#if PIRK_DEV_VARIANTS
     const unsigned int blocks = static_cast<unsigned int>((count + kChainTile - 1) / kChainTile);
     dim3 grid(blocks), block(kChainThreads);
     if (m.kind == kKindTraffic && m.method == kMethodMM)
@@ -507,6 +518,10 @@ cudaError_t launch_chain_step(const ChainModel& m, const WindowArgs& w, const St
     else
         return cudaErrorInvalidValue;
     return cudaGetLastError();
+#else
+    (void)count;
+    return cudaErrorInvalidValue;
+#endif
 }
 
 }  // namespace pirk

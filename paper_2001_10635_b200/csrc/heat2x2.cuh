@@ -17,7 +17,13 @@
 #include <cstdlib>
 
 #include "heat.cuh"
+#ifndef PIRK_DEV_VARIANTS
+#define PIRK_DEV_VARIANTS 0  // 1: also build the rejected A/B variants (4x4 heat blocks, smem chain tiles)
+#endif
+#if PIRK_DEV_VARIANTS
 #include "heat4x4.cuh"
+#endif
+#include <atomic>
 #include "heat_strip.cuh"
 
 namespace pirk {
@@ -613,8 +619,12 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
     // the engine's field-pipelined driver checks that before using them
     if (field_only >= 0 && (Exact || variant != 3 || m.g % 2 != 0)) return cudaErrorInvalidValue;
 
-    static bool attr_set = false;
-    if (!attr_set) {
+    // dynamic shared memory opt-in is per device: once per kernel and device
+    static std::atomic<unsigned long long> attr_done{0};
+    int cur_dev = 0;
+    if (cudaGetDevice(&cur_dev) != cudaSuccess) return cudaErrorInvalidDevice;
+    const unsigned long long dev_bit = 1ull << (cur_dev & 63);
+    if (!(attr_done.load(std::memory_order_acquire) & dev_bit)) {
         cudaError_t e = cudaFuncSetAttribute(heat_step_kernel<Exact>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(kHeatSmemBytes));
@@ -622,9 +632,11 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
             e = cudaFuncSetAttribute(heat2_step_kernel<Exact>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kHeatSmemBytes));
         if constexpr (!Exact) {
+#if PIRK_DEV_VARIANTS
             if (e == cudaSuccess)
                 e = cudaFuncSetAttribute(heat4_step_kernel<Exact>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(k4SmemBytes));
+#endif
             if (e == cudaSuccess)
                 e = cudaFuncSetAttribute(heat_strip_kernel<Exact, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSSmemBytes));
@@ -633,7 +645,7 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSSmemBytes));
         }
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_done.fetch_or(dev_bit, std::memory_order_acq_rel);
     }
     static const int n_sm = [] {
         int dev = 0, v = 148;
@@ -673,6 +685,7 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
             return cudaGetLastError();
         }
         std::memset(&tm, 0, sizeof tm);
+#if PIRK_DEV_VARIANTS
         // 16-byte copies need even g and 16-byte aligned windows
         if (variant == 2 && m.g % 2 == 0 && reinterpret_cast<uintptr_t>(w.in0) % 16 == 0 &&
             reinterpret_cast<uintptr_t>(w.in1) % 16 == 0) {
@@ -684,6 +697,7 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
                                                                                 tm, 1 | (vec ? 2 : 0));
             return cudaGetLastError();
         }
+#endif
     }
     // z chunks: enough CTAs to fill the machine, few enough to keep the
     // 8-plane halo overhead per chunk small.

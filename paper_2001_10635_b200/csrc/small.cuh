@@ -117,20 +117,30 @@ __device__ __forceinline__ void aq_f_all(const SmallModel& m, const double* x, d
 // musl kernels __sin and __cos on [-pi/4, pi/4] (error < 1 ulp of the result
 // there).  CUDA's sincos spends most of its instructions on the general
 // Payne-Hanek path (integer ops and branches: profiles/r01_mc_archquad.txt).
+// The coefficients live in constant memory so the DFMAs read them as
+// constant-bank operands: as immediates every use was rebuilt with two UMOVs
+// (20% of the MC kernel's instructions, profiles/r01_mc_archquad_fast_v3.txt).
+static __constant__ double kSinCos[15] = {
+    0.63661977236758134308,     // 2/pi
+    1.57079632673412561417e+00,  // pio2_1 (33 bits: exact product)
+    6.07710050650619224932e-11,  // pio2_1t
+    8.33333333332248946124e-03, -1.98412698298579493134e-04, 2.75573137070700676789e-06,
+    -2.50507602534068634195e-08, 1.58969099521155010221e-10, -1.66666666666666324348e-01,  // __sin
+    4.16666666666666019037e-02, -1.38888888888741095749e-03, 2.48015872894767294178e-05,
+    -2.75573143513906633035e-07, 2.08757232129817482790e-09, -1.13596475577881948265e-11};  // __cos
 __device__ __forceinline__ void small_sincos(double x, double* s, double* c) {
     if (!(fabs(x) <= 1e5)) {
         sincos(x, s, c);
         return;
     }
-    const double q = rint(x * 0.63661977236758134308);      // 2/pi
-    double r = fma(-q, 1.57079632673412561417e+00, x);      // pio2_1 (33 bits: exact product)
-    r = fma(-q, 6.07710050650619224932e-11, r);             // pio2_1t
+    const double* K = kSinCos;
+    const double q = rint(x * K[0]);
+    double r = fma(-q, K[1], x);
+    r = fma(-q, K[2], r);
     const double z = r * r, w = z * z;
-    const double ps = 8.33333333332248946124e-03 + z * (-1.98412698298579493134e-04 + z * 2.75573137070700676789e-06) +
-                      z * w * (-2.50507602534068634195e-08 + z * 1.58969099521155010221e-10);
-    const double sr = r + (z * r) * (-1.66666666666666324348e-01 + z * ps);
-    const double pc = z * (4.16666666666666019037e-02 + z * (-1.38888888888741095749e-03 + z * 2.48015872894767294178e-05)) +
-                      w * w * (-2.75573143513906633035e-07 + z * (2.08757232129817482790e-09 + z * -1.13596475577881948265e-11));
+    const double ps = K[3] + z * (K[4] + z * K[5]) + z * w * (K[6] + z * K[7]);
+    const double sr = r + (z * r) * (K[8] + z * ps);
+    const double pc = z * (K[9] + z * (K[10] + z * K[11])) + w * w * (K[12] + z * (K[13] + z * K[14]));
     const double hz = 0.5 * z, v = 1.0 - hz;
     const double cr = v + (((1.0 - v) - hz) + z * pc);
     switch (static_cast<int>(q) & 3) {

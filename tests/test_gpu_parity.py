@@ -134,7 +134,7 @@ def test_heat_fast_mode_long_run(fast_ctx):
     assert_within(pk.growth_bound(prob, ctx=fast_ctx), oracle_for("gb", prob))
 
 
-@pytest.mark.parametrize("variant", ["1x2", "2x2", "4x4", "strip"])
+@pytest.mark.parametrize("variant", ["1x2", "2x2", "strip"])
 def test_heat_block_variants(variant):
     """Both heat kernels (1x2 pairs, 2x2 blocks) in both modes: the selector
     (PIRK_HEAT_BLOCK) is read once per process, so each runs in a child."""
@@ -148,7 +148,7 @@ def test_heat_block_variants(variant):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("variant", ["smem", "warp", "warp_single_step"])
+@pytest.mark.parametrize("variant", ["warp", "warp_single_step"])
 def test_chain_kernel_variants(variant):
     """The chain kernels in both modes on the traffic and coupled-chain tests:
     shared-memory tiles, the warp-tiled kernel (default: two RK4 steps per

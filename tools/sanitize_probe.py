@@ -54,7 +54,65 @@ def mc(mode, m_samples=4096):
     ctx.close()
 
 
+def lanes(mode):
+    """Multi-lane context: chain index ranges, heat z-slabs (peer-copy halos,
+    cross-lane events) and Monte Carlo sample ranges on 3 lanes of cuda:0."""
+    ctx = pk.Context(devices=[0, 0, 0], mode=mode)
+    chain_n = 3000
+    m = pk.make_traffic(chain_n)
+    p = pk.ReachProblem(m, pk.IntervalVector(np.full(chain_n, 10.0), np.full(chain_n, 20.0)),
+                        pk.IntervalVector([4.0], [6.0]), 0.0, 2.0, 0.5, 2)
+    pk.mixed_monotonicity(p, ctx=ctx)
+    pk.growth_bound(p, ctx=ctx)
+    g = 40
+    hm = pk.make_heat3d(g)
+    hp = pk.ReachProblem(hm, pk.IntervalVector(np.full(g ** 3, 0.9), np.full(g ** 3, 1.1)), None, 0.0,
+                         3 * 1e-4, 1e-4, 1)
+    pk.mixed_monotonicity(hp, ctx=ctx)
+    ll = pk.make_laub_loomis()
+    c = np.array([1.2, 1.05, 1.5, 2.4, 1.0, 0.1, 0.45])
+    p2 = pk.ReachProblem(ll, pk.IntervalVector(c - 0.05, c + 0.05), None, 0.0, 0.1, 0.01, 5)
+    pk.monte_carlo(p2, pk.MonteCarloSpec(seed=1, samples_override=3000), ctx=ctx)
+    ctx.close()
+
+
+USER_SRC = r"""
+__device__ double pirk_rhs(u64 i, double, const double* x, const double* p) {
+    const double l = i > 0 ? x[i - 1] : p[0];
+    const double r = i + 1 < PIRK_N ? x[i + 1] : 0.0;
+    return 0.5 * (l - x[i]) - 0.25 * (x[i] - r) / (1.0 + x[i] * x[i]);
+}
+__device__ double pirk_decomposition(u64 i, double t, const double* x, const double* p, const double*,
+                                     const double*) { return pirk_rhs(i, t, x, p); }
+__device__ double pirk_growth(u64 i, double, const double* r, const double* w) {
+    return 0.5 * (i > 0 ? r[i - 1] : w[0]) + 0.25 * (i + 1 < PIRK_N ? r[i + 1] : 0.0);
+}
+"""
+
+
+def user(mode):
+    """NVRTC user-model kernels: one-thread (n <= 64), per-component stage
+    (n > 64) and Monte Carlo, plus the catalog MC beyond 64 components."""
+    ctx = pk.Context(0, mode)
+    for n in (12, 300):
+        m = pk.make_user_model(USER_SRC, n, 1, decomposition=True, growth=True, input_affine=True)
+        p = pk.ReachProblem(m, pk.IntervalVector(np.zeros(n), np.ones(n)), pk.IntervalVector([0.5], [1.0]),
+                            0.0, 0.2, 0.05, 2)
+        pk.mixed_monotonicity(p, ctx=ctx)
+        pk.growth_bound(p, ctx=ctx)
+        pk.monte_carlo(p, pk.MonteCarloSpec(seed=2, samples_override=700), ctx=ctx)
+    tm = pk.make_traffic(100)
+    tp = pk.ReachProblem(tm, pk.IntervalVector(np.full(100, 10.0), np.full(100, 20.0)),
+                         pk.IntervalVector([4.0], [6.0]), 0.0, 1.0, 0.5, 1)
+    pk.monte_carlo(tp, pk.MonteCarloSpec(seed=2, samples_override=500), ctx=ctx)
+    ctx.close()
+
+
 CASES = {
+    "lanes_exact": lambda: lanes("exact"),
+    "lanes_fast": lambda: lanes("fast"),
+    "user_exact": lambda: user("exact"),
+    "user_fast": lambda: user("fast"),
     "heat_fast": lambda: heat("fast", 130),
     "heat_exact": lambda: heat("exact", 72),
     "chain_fast": lambda: chain("fast", "chain"),
