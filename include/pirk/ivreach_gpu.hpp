@@ -125,10 +125,17 @@ struct SystemModel {
     std::size_t input_dim = 0;
     bool input_affine = true;
     std::string sparsity_note;
+    // user-defined evaluators (make_user_model); shared by copies of the model
+    std::shared_ptr<pirk_program> program;
     bool has_growth() const {
+        if (desc.kind == PIRK_USER) return user_flags & PIRK_HAS_GROWTH;
         return desc.kind != PIRK_CHAIN;
     }
-    bool has_decomposition() const { return desc.decomp != PIRK_DECOMP_NONE; }
+    bool has_decomposition() const {
+        if (desc.kind == PIRK_USER) return user_flags & PIRK_HAS_DECOMPOSITION;
+        return desc.decomp != PIRK_DECOMP_NONE;
+    }
+    std::uint32_t user_flags = 0;
 };
 
 struct ReachProblem {
@@ -192,6 +199,34 @@ inline SystemModel make_scalar_decay() { return detail::make(PIRK_SCALAR_DECAY, 
 inline SystemModel make_scalar_linear(double a = 1.0) {
     return detail::make(PIRK_SCALAR_LINEAR, 1, 0, {a}, PIRK_DECOMP_NATIVE);
 }
+// A model with caller-written evaluators -- the reference's SystemModel built
+// from arbitrary std::function rhs / decomposition / growth_rhs
+// (system_model.hpp:14-43) -- as CUDA device functions with the same arguments:
+//
+//   __device__ double pirk_rhs(u64 i, double t, const double* x, const double* p);
+//   __device__ double pirk_decomposition(u64 i, double t, const double* x, const double* p,
+//                                        const double* xh, const double* ph);
+//   __device__ double pirk_growth(u64 i, double t, const double* r, const double* w);
+//
+// compiled by NVRTC for sm_100a on first use (pirk_c.h).  A source that does
+// not compile is reported by the entry points as std::invalid_argument with
+// the compiler's log.
+inline SystemModel make_user_model(const std::string& source, std::size_t dim, std::size_t input_dim,
+                                   bool has_decomposition, bool has_growth, bool input_affine) {
+    detail::require(dim >= 1, "user model needs at least 1 state");
+    const std::uint32_t flags = PIRK_HAS_RHS | (has_decomposition ? PIRK_HAS_DECOMPOSITION : 0u) |
+                                (has_growth ? PIRK_HAS_GROWTH : 0u) | (input_affine ? PIRK_INPUT_AFFINE : 0u);
+    pirk_program* raw = nullptr;
+    if (pirk_program_create(source.c_str(), dim, input_dim, flags, &raw) != PIRK_OK)
+        throw std::invalid_argument("user model: invalid source or dimension");
+    SystemModel m = detail::make(PIRK_USER, dim, input_dim, {}, has_decomposition ? PIRK_DECOMP_NATIVE : PIRK_DECOMP_NONE);
+    m.program.reset(raw, pirk_program_destroy);
+    m.desc.program = raw;
+    m.user_flags = flags;
+    m.input_affine = input_affine;
+    return m;
+}
+
 // User-supplied decomposition d_i = f_i(x) + sum_{j!=i} C_ij (x_j - xh_j) (see pirk_c.h).
 inline SystemModel with_jacobian_decomposition(SystemModel m) {
     m.desc.decomp = PIRK_DECOMP_JACOBIAN;

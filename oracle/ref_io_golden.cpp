@@ -10,11 +10,19 @@
 //   synthetic.json         : a hand-built tube exercising nlohmann's double
 //                            formatting (tiny, huge, negative, integral values)
 //   bench.csv              : bench_csv over three synthetic rows
+//   configs/<name>.parsed  : serialize_config(parse_config_file(proj/configs/<name>.cfg))
+//   configs/errors.tsv     : parse_config's invalid_argument message per bad config text
+//   configs/<name>.json    : run_config's tube file (and .report.json) for the
+//                            configs the device library supports (`<dir> configs <cfgdir>`)
 #include <cstdio>
 #include <fstream>
 #include <string>
 #include <vector>
 
+#include <filesystem>
+#include <stdexcept>
+
+#include "ivreach/config.hpp"
 #include "ivreach/driver.hpp"
 #include "ivreach/io.hpp"
 #include "ivreach/models.hpp"
@@ -27,8 +35,56 @@ static void put(const std::string& dir, const std::string& name, const std::stri
     f << text;
 }
 
+static int configs(const std::string& dir, const std::string& cfgdir) {
+    namespace fs = std::filesystem;
+    fs::create_directories(dir);
+    for (const auto& e : fs::directory_iterator(cfgdir)) {
+        if (e.path().extension() != ".cfg") continue;
+        const std::string name = e.path().stem().string();
+        RunConfig cfg = parse_config_file(e.path().string());
+        put(dir, name + ".parsed", serialize_config(cfg));
+        static const char* runnable[] = {"traffic", "heat3d", "laub-loomis", "arch-quadrotor", "vdp",
+                                         "vdp-mc", "scalar-decay", "scalar-linear"};
+        bool run = false;
+        for (const char* r : runnable) run = run || name == r;
+        if (!run) continue;
+        cfg.output = dir + "/" + name;
+        cfg.workers = 1;
+        run_config(cfg);
+    }
+    // parse errors (config.cpp messages, with line numbers)
+    const std::vector<std::pair<std::string, std::string>> bad = {
+        {"no_model", "method = growth-bound\n"},
+        {"unknown_key", "model = vdp\ncolour = red\n"},
+        {"no_equals", "model = vdp\njust words\n"},
+        {"unknown_model", "model = banana\n"},
+        {"unknown_param", "model = vdp\nparam.nope = 1\n"},
+        {"bad_number", "model = vdp\nt1 = 1.0x\n"},
+        {"bad_method", "model = vdp\nmethod = magic\n"},
+        {"unsupported_method", "model = vdp\nmethod = mixed-monotonicity\n"},
+        {"box_length", "model = vdp\ninitial.lower = 1, 2, 3\n"},
+        {"inputs_on_autonomous", "model = vdp\ninput.lower = 1\n"},
+        {"negative_stride", "model = vdp\ntube_stride = -1\n"},
+        {"epsilon_range", "model = vdp\nepsilon = 1.5\n"},
+        {"bad_format", "model = vdp\nformat = xml\n"},
+        {"bad_grid", "model = heat3d\nparam.grid = 2.5\n"},
+        {"empty_param", "model = vdp\nparam. = 1\n"},
+        {"empty_vector", "model = traffic\ninitial.lower = \n"},
+        {"too_many_workers", "model = vdp\nworkers = 5000\n"},
+    };
+    std::string tsv;
+    for (const auto& [k, text] : bad) {
+        std::string msg = "(no error)";
+        try { parse_config(text); } catch (const std::invalid_argument& e) { msg = e.what(); }
+        tsv += k + "\t" + msg + "\n";
+    }
+    put(dir, "errors.tsv", tsv);
+    return 0;
+}
+
 int main(int argc, char** argv) {
     const std::string dir = argc > 1 ? argv[1] : ".";
+    if (argc > 3 && std::string(argv[2]) == "configs") return configs(dir, argv[3]);
     SystemModel m = make_traffic(5);
     ReachProblem p{m, IntervalVector(std::vector<double>(5, 10.0), std::vector<double>(5, 20.0)),
                    IntervalVector(std::vector<double>{4.0}, std::vector<double>{6.0}), 0.0, 3.0, 0.5, 2};

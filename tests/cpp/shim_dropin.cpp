@@ -116,5 +116,30 @@ int main(int argc, char** argv) {
         for (std::size_t k = 0; same && k < a.entries.size(); ++k) same = a.entries[k].box == b.entries[k].box;
         check(same, "laub-loomis MC: workers 3 == workers 1");
     }
+    {   // test_reach.cpp:190-206 through the shim: a user decomposition that
+        // violates the embedding order is a runtime_error, as in the reference
+        const std::string src = R"(
+__device__ double pirk_rhs(u64 i, double, const double* x, const double*) { return i == 0 ? x[1] : -1.0; }
+__device__ double pirk_decomposition(u64 i, double, const double*, const double*, const double* xh,
+                                     const double*) { return i == 0 ? xh[1] : -1.0; })";
+        SystemModel m = make_user_model(src, 2, 0, true, false, false);
+        ReachProblem p{m, IntervalVector({0.0, 0.0}, {1.0, 0.5}), std::nullopt, 0.0, 3.0, 0.1, 1};
+        bool threw = false;
+        try { mixed_monotonicity(p, 1); } catch (const std::runtime_error& e) {
+            threw = std::string(e.what()) == "mixed-monotonicity: embedding order violated at step 20, t = 2.000000, component 0";
+        }
+        check(threw, "user model: order-violating decomposition -> runtime_error (reference message)");
+        bool invalid = false;
+        try { growth_bound(p, 1); } catch (const std::invalid_argument&) { invalid = true; }
+        check(invalid, "user model without growth_rhs: growth_bound -> invalid_argument");
+        SystemModel bad = make_user_model("__device__ double pirk_rhs(u64, double, const double*, const double*) { return nope; }",
+                                          1, 0, false, false, false);
+        ReachProblem pb{bad, IntervalVector({0.0}, {1.0}), std::nullopt, 0.0, 1.0, 0.1, 0};
+        bool bad_src = false;
+        try { monte_carlo(pb, MonteCarloSpec{}, 1); } catch (const std::invalid_argument& e) {
+            bad_src = std::string(e.what()).find("nope") != std::string::npos;
+        }
+        check(bad_src, "user model that does not compile -> invalid_argument with the NVRTC log");
+    }
     return failures;
 }
