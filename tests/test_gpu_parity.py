@@ -285,7 +285,7 @@ def test_traffic_mc_exact_and_seeded(ctx):
 def test_arch_quad_mc_tolerance(ctx):
     m, prob = arch_quad_problem()
     tube = pk.monte_carlo(prob, pk.MonteCarloSpec(seed=1, samples_override=4096), ctx=ctx)
-    assert_within(tube, mc_oracle(prob, 1, 4096), rel=1e-12, atol=1e-14, never_tighter=False)
+    assert_within(tube, mc_oracle(prob, 1, 4096), rel=1e-12, atol=1e-14)
 
 
 def test_arch_quad_mc_fast_mode_tolerance(fast_ctx):
@@ -293,7 +293,7 @@ def test_arch_quad_mc_fast_mode_tolerance(fast_ctx):
     field (csrc/small.cuh aq_f_all_fast), against the glibc-trig oracle."""
     m, prob = arch_quad_problem()
     tube = pk.monte_carlo(prob, pk.MonteCarloSpec(seed=1, samples_override=4096), ctx=fast_ctx)
-    assert_within(tube, mc_oracle(prob, 1, 4096), rel=1e-12, atol=1e-14, never_tighter=False)
+    assert_within(tube, mc_oracle(prob, 1, 4096), rel=1e-12, atol=1e-14)
 
 
 def test_mc_hull_inside_exact_image(ctx):
@@ -415,7 +415,7 @@ def test_cuda_matches_reference_golden(ctx, case):
         tube = pk.monte_carlo(prob, pk.MonteCarloSpec(seed=kw["seed"], samples_override=kw["samples"]),
                               ctx=ctx)
     if model.kind == pk.ARCH_QUAD:  # CUDA sin/cos vs glibc: tolerance contract
-        assert_within(tube, R, rel=1e-12, atol=1e-14, never_tighter=(method != O.METHOD_MC))
+        assert_within(tube, R, rel=1e-12, atol=1e-14)
     else:
         assert_bitexact(tube, R)
 

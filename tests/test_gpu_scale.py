@@ -289,7 +289,7 @@ def test_c2_arch_quad_mc_m1e6_vs_reference():
         finally:
             c.close()
         assert tube.report.m == 10 ** 6
-        assert_within(tube, ref, rel=1e-12, atol=1e-14, never_tighter=False)
+        assert_within(tube, ref, rel=1e-12, atol=1e-14)
 
 
 def test_c2_laub_loomis_mc_m1e6_bitexact():

@@ -225,7 +225,7 @@ def test_user_traffic_equals_catalog(mctx, n):
         if mctx.mode == "exact":
             assert_bitexact(tube, oref)
         else:
-            assert_within(tube, oref, rel=1e-12, never_tighter=False)
+            assert_within(tube, oref, rel=1e-12)
 
 
 def test_user_mc_equals_catalog(ctx):
