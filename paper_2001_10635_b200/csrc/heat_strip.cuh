@@ -76,6 +76,15 @@
 #if PIRK_STRIP_LADDER && !PIRK_STRIP_SPLITBAR
 #error "PIRK_STRIP_LADDER needs PIRK_STRIP_SPLITBAR"
 #endif
+#ifndef PIRK_STRIP_SANITIZE
+// 1 (racecheck builds only): the halo warps' reads of the rows outside the
+// footprint (warp 0's row -1, warp 15's row 64) go to a private dummy row
+// instead of wrapping into the exchange region / the next x slot.  Those
+// values only ever feed halo cells (garbage by design, never stored), so the
+// wrap is benign -- but racecheck reports it; with this on, any remaining
+// hazard would be a real one.
+#define PIRK_STRIP_SANITIZE 0
+#endif
 #ifndef PIRK_STRIP_S4SKIP
 #define PIRK_STRIP_S4SKIP 0  // halo warps 0 and 15 skip stage 4 (measured slower: 7.40 vs 6.55 ms, g=800)
 #endif
@@ -178,16 +187,31 @@ struct HeatStrip {
     }
 
     // rows above / below the block: from the x slot (stage 1) or a level
+    __device__ __forceinline__ const double* dummy_row() const {
+        return XR + kSXSlots * kSXSlot + 2 * (t & 31);  // the padding row after the ring
+    }
     __device__ __forceinline__ void x_tb(const double* X, double (&T)[2], double (&B)[2]) const {
-        const double2 a = *reinterpret_cast<const double2*>(X + xo - kSF);
-        const double2 c = *reinterpret_cast<const double2*>(X + xo + 4 * kSF);
+        const double* pa = X + xo - kSF;
+        const double* pc = X + xo + 4 * kSF;
+        if constexpr (PIRK_STRIP_SANITIZE) {
+            if (t < 32) pa = dummy_row();
+            if (t >= kSThreads - 32) pc = dummy_row();
+        }
+        const double2 a = *reinterpret_cast<const double2*>(pa);
+        const double2 c = *reinterpret_cast<const double2*>(pc);
         T[0] = a.x, T[1] = a.y, B[0] = c.x, B[1] = c.y;
     }
     // exchange buffer `buf` (iteration parity) of level 0..2 (u1..u3)
     __device__ __forceinline__ void u_tb(int buf, int level, double (&T)[2], double (&B)[2]) const {
         const double2* L = EX + (3 * buf + level) * kSLevel;
-        const double2 a = L[kSThreads + t - 32];  // BOT of the block above
-        const double2 c = L[t + 32];              // TOP of the block below
+        const double2* pa = L + kSThreads + t - 32;  // BOT of the block above
+        const double2* pc = L + t + 32;              // TOP of the block below
+        if constexpr (PIRK_STRIP_SANITIZE) {
+            if (t < 32) pa = reinterpret_cast<const double2*>(dummy_row());
+            if (t >= kSThreads - 32) pc = reinterpret_cast<const double2*>(dummy_row());
+        }
+        const double2 a = *pa;
+        const double2 c = *pc;
         T[0] = a.x, T[1] = a.y, B[0] = c.x, B[1] = c.y;
     }
     __device__ __forceinline__ void publish(int buf, int level, const double (&v)[8]) const {

@@ -103,39 +103,34 @@ class HaloExchanger:
 
     def start(self, fields):
         """Post the halo sends / receives and return a handle for finish().  The
-        sends read the owned boundary units in place; the received halos land
-        in separate buffers, so the window may be read (not written) meanwhile:
-        on GPUs NCCL moves the halos while the interior of the next step runs."""
+        sends read the owned boundary units in place and the receives land
+        straight in the window's halo slices (contiguous views: no staging
+        buffer, no copy), so the window's owned units may be read meanwhile:
+        on GPUs NCCL moves the halos while the interior of the step runs (its
+        4-unit stencil cone stays inside the owned units)."""
         s = self.shard
         H = s.halo
         u = self.unit
         ops = []
         left, right = s.rank - 1, s.rank + 1
         wb = s.win_begin
-        recv = []
         for f in fields:
             if left >= 0:
-                snd = f[(s.begin - wb) * u:(s.begin - wb + H) * u].contiguous()
-                rcv = f.new_empty((s.begin - s.win_begin) * u)
+                snd = f[(s.begin - wb) * u:(s.begin - wb + H) * u]
+                rcv = f[0:(s.begin - wb) * u]
                 ops.append(self.dist.P2POp(self.dist.isend, snd, left, self.group))
                 ops.append(self.dist.P2POp(self.dist.irecv, rcv, left, self.group))
-                recv.append((f, 0, rcv))
             if right < s.world:
-                snd = f[(s.end - wb - H) * u:(s.end - wb) * u].contiguous()
-                rcv = f.new_empty((s.win_end - s.end) * u)
+                snd = f[(s.end - wb - H) * u:(s.end - wb) * u]
+                rcv = f[(s.end - wb) * u:(s.win_end - wb) * u]
                 ops.append(self.dist.P2POp(self.dist.isend, snd, right, self.group))
                 ops.append(self.dist.P2POp(self.dist.irecv, rcv, right, self.group))
-                recv.append((f, (s.end - wb) * u, rcv))
-        reqs = self.dist.batch_isend_irecv(ops) if ops else []
-        return reqs, recv
+        return self.dist.batch_isend_irecv(ops) if ops else []
 
     def finish(self, handle):
-        """Wait for the exchange and copy the received halos into the window."""
-        reqs, recv = handle
-        for r in reqs:
+        """Wait for the exchange (the halos are already in place)."""
+        for r in handle:
             r.wait()
-        for f, off, rcv in recv:
-            f[off:off + rcv.numel()].copy_(rcv)
 
 
 def device_step_fn(model: SystemModel, method: str, ctx=None):
