@@ -192,6 +192,18 @@ int32_t pirk_lane_count(const pirk_ctx* ctx);
 /* Visible CUDA devices (0 when there is none). */
 int32_t pirk_device_count(void);
 int32_t pirk_lane_device(const pirk_ctx* ctx, int32_t lane);
+/* Streaming observer (StepObserver, rk4.hpp:63-64, called as rk4.cpp:106-111
+ * does): when set, every run on the context calls fn once per recorded slot,
+ * in slot order, with that slot's box (MM: x / x-hat; GB: the clamped box; MC:
+ * the hull) in host memory valid for the duration of the call.  For chain /
+ * heat3d / user models the callback for slot s runs while the device
+ * integrates towards slot s+1, so a tube larger than host memory can be
+ * consumed slot by slot (pirk_tube.lower / .upper may then be NULL).  A run
+ * that fails delivers the slots recorded before the failure was detected and
+ * then returns the error.  fn = NULL disables it. */
+typedef void (*pirk_record_fn)(void* user, uint64_t slot, uint64_t step, double t, const double* lower,
+                               const double* upper, uint64_t n);
+pirk_status pirk_set_record_callback(pirk_ctx* ctx, pirk_record_fn fn, void* user);
 /* Free the state buffers a context keeps between runs of the same size. */
 pirk_status pirk_release_cache(pirk_ctx* ctx);
 void pirk_destroy(pirk_ctx* ctx);

@@ -112,6 +112,7 @@ SIGNATURES = {
     "pirk_device_count": (C.c_int32, []),
     "pirk_lane_device": (C.c_int32, [C.c_void_p, C.c_int32]),
     "pirk_release_cache": (C.c_int, [C.c_void_p]),
+    "pirk_set_record_callback": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "pirk_destroy": (None, [C.c_void_p]),
     "pirk_last_error": (C.c_char_p, [C.c_void_p]),
     "pirk_set_mode": (C.c_int, [C.c_void_p, C.c_int32]),
@@ -142,6 +143,10 @@ SIGNATURES = {
     "pirk_step_window": (C.c_int, [C.c_void_p, _MP, C.c_int32, C.POINTER(PirkWindow), _DP, _DP,
                                    C.c_double, C.c_double, C.c_uint64, C.c_void_p]),
 }
+
+# pirk_record_fn (include/pirk_c.h)
+RECORD_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_uint64, C.c_uint64, C.c_double, C.POINTER(C.c_double),
+                        C.POINTER(C.c_double), C.c_uint64)
 
 _lib = None
 _lock = threading.Lock()

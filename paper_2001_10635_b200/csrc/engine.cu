@@ -85,6 +85,9 @@ struct pirk_ctx {
     // size: freeing 4 x 32 GB costs up to ~0.5 s of unmapping per call
     std::vector<CachedBlock> cache;
     std::vector<PirkLane> peers;  // lanes 1 .. W-1 (empty for a one-device context)
+    // streaming observer (pirk_set_record_callback): called per recorded slot
+    pirk_record_fn record_fn = nullptr;
+    void* record_user = nullptr;
     // catalog vector fields as generated NVRTC sources (Monte Carlo with
     // n > kSmallMax, user_models.cuh), keyed by source
     std::map<std::string, std::unique_ptr<pirk_program>> catalog_programs;
@@ -781,9 +784,73 @@ pirk_status run_heat_mm_pipelined(pirk_ctx* ctx, const pirk_model* m, const pirk
         return fail(ctx, PIRK_EORDER, "mixed-monotonicity: embedding order violated at step " +
                                           std::to_string(e.plan.total) + ", t = " + fstr(p->t1) +
                                           ", component " + std::to_string(hf[3]));
+    if (ctx->record_fn) ctx->record_fn(ctx->record_user, 0, e.plan.total, p->t1, tube->lower, tube->upper, n);
     fill_report(rep, n, 0, e.plan.total, 7 * 2 * n * sizeof(double), 4 * n * sizeof(double), exact_mode(ctx),
                 setup_s, integ_s, 0.0, ctx->launches - launches0);
     return PIRK_OK;
+}
+
+// Streams recorded slots to the context's record callback (the StepObserver of
+// rk4.hpp:63-64, invoked at rk4.cpp:106-111): slot s's box is copied into one
+// page-locked staging buffer (lower | upper) on the lanes' streams, and the
+// callback for slot s runs on the host while the device integrates towards
+// slot s+1 -- the driver enqueues those steps before delivering s.  Order per
+// slot: steps(s+1) enqueued, deliver(s) (waits for copy(s), calls back), then
+// copy(s+1) may reuse the buffer.
+struct SlotStreamer {
+    pirk_ctx* ctx = nullptr;
+    uint64_t n = 0;
+    double* buf = nullptr;  // pinned, 2n
+    std::vector<cudaEvent_t> ev;
+    int64_t pending = -1;
+    uint64_t pend_step = 0;
+    double pend_t = 0.0;
+    bool on() const { return buf != nullptr; }
+    cudaError_t init(pirk_ctx* c, uint64_t n_, int lanes) {
+        ctx = c;
+        n = n_;
+        if (!c->record_fn) return cudaSuccess;
+        cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&buf), 2 * n * sizeof(double));
+        if (e != cudaSuccess) {
+            buf = nullptr;
+            return e;
+        }
+        ev.assign(static_cast<size_t>(lanes), nullptr);
+        for (cudaEvent_t& x : ev)
+            if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) return e;
+        return cudaSuccess;
+    }
+    // the slot's copies are enqueued on lane r's stream: mark them
+    cudaError_t mark(int r, cudaStream_t st) { return cudaEventRecord(ev[static_cast<size_t>(r)], st); }
+    cudaError_t deliver() {
+        if (pending < 0) return cudaSuccess;
+        for (cudaEvent_t x : ev) {
+            const cudaError_t e = cudaEventSynchronize(x);
+            if (e != cudaSuccess) return e;
+        }
+        ctx->record_fn(ctx->record_user, static_cast<uint64_t>(pending), pend_step, pend_t, buf, buf + n, n);
+        pending = -1;
+        return cudaSuccess;
+    }
+    void set_pending(uint64_t s, uint64_t step, double t) {
+        pending = static_cast<int64_t>(s);
+        pend_step = step;
+        pend_t = t;
+    }
+    ~SlotStreamer() {
+        for (cudaEvent_t x : ev)
+            if (x) cudaEventDestroy(x);
+        if (buf) cudaFreeHost(buf);
+    }
+};
+
+// Host-side tubes (small systems, Monte Carlo): every slot to the callback
+// after the run, from host memory.
+void stream_host_tube(pirk_ctx* ctx, const std::vector<uint64_t>& slot_steps, const std::vector<double>& slot_times,
+                      const double* lower, const double* upper, uint64_t n) {
+    if (!ctx->record_fn || !lower || !upper) return;
+    for (uint64_t s = 0; s < slot_steps.size(); ++s)
+        ctx->record_fn(ctx->record_user, s, slot_steps[s], slot_times[s], lower + s * n, upper + s * n, n);
 }
 
 // The error contract of a finished large-model run, in the reference's order
@@ -886,9 +953,12 @@ pirk_status run_large(pirk_ctx* ctx, const pirk_model* m, int method, const pirk
 
     const auto t_int = Clock::now();
     const uint64_t n = e.n;
+    SlotStreamer rec;
+    CK(ctx, rec.init(ctx, n, 1));
     for (uint64_t s = 0; s < S; ++s) {
         st = engine_advance(&e, slot_steps[s] - e.done);
         if (st != PIRK_OK) return st;
+        CK(ctx, rec.deliver());  // slot s-1 to the callback while these steps run
         const double* out_lo = e.s0();
         const double* out_hi = e.s1();
         if (method == PIRK_METHOD_MM) {
@@ -906,7 +976,14 @@ pirk_status run_large(pirk_ctx* ctx, const pirk_model* m, int method, const pirk
             CK(ctx, cudaMemcpyAsync(tube->lower + s * n, out_lo, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         if (tube && tube->upper)
             CK(ctx, cudaMemcpyAsync(tube->upper + s * n, out_hi, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        if (rec.on()) {
+            CK(ctx, cudaMemcpyAsync(rec.buf, out_lo, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+            CK(ctx, cudaMemcpyAsync(rec.buf + n, out_hi, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+            CK(ctx, rec.mark(0, ctx->stream));
+            rec.set_pending(s, slot_steps[s], slot_times[s]);
+        }
     }
+    CK(ctx, rec.deliver());
     std::vector<unsigned long long> flags(S);
     std::vector<double> vals(S);
     CK(ctx, cudaMemcpyAsync(ctx->h_flags, e.d_fail.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1064,6 +1141,8 @@ pirk_status run_large_multi(pirk_ctx* ctx, const pirk_model* m, int method, cons
                   : launch_heat_step<false>(hm, w, sc, k, z.fail.p, z.L.s);
     };
     const size_t halo_bytes = 4 * unit * sizeof(double);
+    SlotStreamer rec;
+    CK(ctx, rec.init(ctx, n, W));
     uint64_t done = 0;
     for (uint64_t s = 0; s < S; ++s) {
         for (; done < slot_steps[s]; ++done) {
@@ -1103,6 +1182,7 @@ pirk_status run_large_multi(pirk_ctx* ctx, const pirk_model* m, int method, cons
             }
             for (int r = 0; r < W; ++r) sh[static_cast<size_t>(r)].cur ^= 1;
         }
+        CK(ctx, rec.deliver());  // slot s-1 to the callback while these steps run
         for (int r = 0; r < W; ++r) {  // record slot s on every lane's owned units
             ShardState& z = sh[static_cast<size_t>(r)];
             CK(ctx, cudaSetDevice(z.L.device));
@@ -1123,8 +1203,16 @@ pirk_status run_large_multi(pirk_ctx* ctx, const pirk_model* m, int method, cons
                 CK(ctx, cudaMemcpyAsync(tube->lower + s * n + z.b * unit, lo, cnt * sizeof(double), cudaMemcpyDeviceToHost, z.L.s));
             if (tube && tube->upper)
                 CK(ctx, cudaMemcpyAsync(tube->upper + s * n + z.b * unit, hi, cnt * sizeof(double), cudaMemcpyDeviceToHost, z.L.s));
+            if (rec.on()) {
+                CK(ctx, cudaMemcpyAsync(rec.buf + z.b * unit, lo, cnt * sizeof(double), cudaMemcpyDeviceToHost, z.L.s));
+                CK(ctx, cudaMemcpyAsync(rec.buf + n + z.b * unit, hi, cnt * sizeof(double), cudaMemcpyDeviceToHost, z.L.s));
+                CK(ctx, rec.mark(r, z.L.s));
+            }
         }
+        if (rec.on()) rec.set_pending(s, slot_steps[s], slot_times[s]);
     }
+    CK(ctx, cudaSetDevice(ctx->device));
+    CK(ctx, rec.deliver());
     unsigned long long f0 = kNoFail, f1 = kNoFail, box = kNoFail;
     std::vector<unsigned long long> flags(S, kNoFail), lf(S);
     std::vector<double> vals(S, 0.0), lv(S);
@@ -1282,6 +1370,7 @@ pirk_status run_small(pirk_ctx* ctx, const pirk_model* m, int method, const pirk
                                                       ", component " + std::to_string(i));
             if (tube && tube->lower) std::memcpy(tube->lower + s * n, xx, n * sizeof(double));
             if (tube && tube->upper) std::memcpy(tube->upper + s * n, xx + n, n * sizeof(double));
+            if (ctx->record_fn) ctx->record_fn(ctx->record_user, s, slot_steps[s], slot_times[s], xx, xx + n, n);
         }
         fill_report(rep, n, 0, plan.total, 7 * 2 * n * sizeof(double), 4 * 2 * n * sizeof(double),
                     ex, setup_s, integ_s, since(t_red), ctx->launches - launches0);
@@ -1310,6 +1399,14 @@ pirk_status run_small(pirk_ctx* ctx, const pirk_model* m, int method, const pirk
                 }
                 if (tube && tube->lower) tube->lower[s * n + i] = c[i] - r[i];
                 if (tube && tube->upper) tube->upper[s * n + i] = c[i] + r[i];
+            }
+            if (ctx->record_fn) {
+                std::vector<double> lo(n), hi(n);
+                for (uint64_t i = 0; i < n; ++i) {
+                    lo[i] = c[i] - r[i];
+                    hi[i] = c[i] + r[i];
+                }
+                ctx->record_fn(ctx->record_user, s, slot_steps[s], slot_times[s], lo.data(), hi.data(), n);
             }
         }
         fill_report(rep, n, 0, plan.total, 7 * n * sizeof(double), 4 * n * sizeof(double), ex,
@@ -1460,10 +1557,15 @@ pirk_status run_mc(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p, ui
         *fraction = static_cast<double>(outside) / static_cast<double>(count);
         return PIRK_OK;
     }
+    std::vector<double> slo, shi;  // the record callback's copy of a slot
     if (tube) {
         tube->n_slots = S;
         for (uint64_t s = 0; s < S; ++s) {
             if (tube->times) tube->times[s] = slot_times[s];
+            if (ctx->record_fn && !fold_into) {
+                slo.assign(n, 0.0);
+                shi.assign(n, 0.0);
+            }
             for (uint64_t i = 0; i < n; ++i) {
                 unsigned long long klo = ln[0].hull[s * 2 * n + i], khi = ln[0].hull[s * 2 * n + n + i];
                 for (int r = 1; r < W; ++r) {  // HullAccumulator::merge (reach.cpp:232-241) on keys
@@ -1479,7 +1581,12 @@ pirk_status run_mc(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p, ui
                     if (tube->lower) tube->lower[s * n + i] = lo;
                     if (tube->upper) tube->upper[s * n + i] = hi;
                 }
+                if (!slo.empty()) {
+                    slo[i] = lo;
+                    shi[i] = hi;
+                }
             }
+            if (!slo.empty()) ctx->record_fn(ctx->record_user, s, slot_steps[s], slot_times[s], slo.data(), shi.data(), n);
         }
     }
     // reach.cpp:273-275 with `outer` = lanes
@@ -1568,6 +1675,14 @@ int32_t pirk_device_count(void) {
 int32_t pirk_lane_device(const pirk_ctx* ctx, int32_t lane) {
     if (!ctx || lane < 0 || lane >= ctx->lanes()) return -1;
     return lane == 0 ? ctx->device : ctx->peers[static_cast<size_t>(lane - 1)].device;
+}
+
+pirk_status pirk_set_record_callback(pirk_ctx* ctx, pirk_record_fn fn, void* user) {
+    if (!ctx) return PIRK_EINVAL;
+    LOCK(ctx);
+    ctx->record_fn = fn;
+    ctx->record_user = user;
+    return PIRK_OK;
 }
 
 pirk_status pirk_release_cache(pirk_ctx* ctx) {

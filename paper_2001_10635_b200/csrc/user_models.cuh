@@ -138,6 +138,8 @@ pirk_status run_user_large(pirk_ctx* ctx, const pirk_model* m, int method, const
     CK(ctx, cudaMemsetAsync(dfail.p, 0xff, 2 * sizeof(unsigned long long), ctx->stream));
     CK(ctx, cudaMemsetAsync(sflag.p, 0xff, S * sizeof(unsigned long long), ctx->stream));
     std::vector<double> hc, hr;  // GB: host centres and radii, slots x n
+    SlotStreamer rec;  // MM: slots stream to the record callback during the run
+    if (mm) CK(ctx, rec.init(ctx, n, 1));
     const double setup_s = since(t_setup);
     const auto t_int = Clock::now();
     for (int pass = 0; pass < (mm ? 1 : 2); ++pass) {
@@ -176,12 +178,18 @@ pirk_status run_user_large(pirk_ctx* ctx, const pirk_model* m, int method, const
                 }
             }
             if (mm) {
+                CK(ctx, rec.deliver());
                 CK(ctx, launch_order_check(X.p, X.p + n, n, sflag.p + s, ctx->stream));  // reach.cpp:181-186
                 ctx->launches++;
                 if (tube && tube->lower)
                     CK(ctx, cudaMemcpyAsync(tube->lower + s * n, X.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
                 if (tube && tube->upper)
                     CK(ctx, cudaMemcpyAsync(tube->upper + s * n, X.p + n, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+                if (rec.on()) {
+                    CK(ctx, cudaMemcpyAsync(rec.buf, X.p, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+                    CK(ctx, rec.mark(0, ctx->stream));
+                    rec.set_pending(s, slot_steps[s], slot_times[s]);
+                }
             } else {
                 double* dst = (pass == 0 ? hc : hr).data() + s * n;
                 CK(ctx, cudaMemcpyAsync(dst, X.p, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -189,6 +197,7 @@ pirk_status run_user_large(pirk_ctx* ctx, const pirk_model* m, int method, const
         }
         CK(ctx, cudaStreamSynchronize(ctx->stream));
     }
+    CK(ctx, rec.deliver());
     unsigned long long hf[2];
     std::vector<unsigned long long> flags(S);
     CK(ctx, cudaMemcpyAsync(hf, dfail.p, sizeof hf, cudaMemcpyDeviceToHost, ctx->stream));
@@ -218,6 +227,14 @@ pirk_status run_user_large(pirk_ctx* ctx, const pirk_model* m, int method, const
                 for (uint64_t i = 0; i < n; ++i) tube->lower[s * n + i] = hc[s * n + i] - hr[s * n + i];
             if (tube && tube->upper)
                 for (uint64_t i = 0; i < n; ++i) tube->upper[s * n + i] = hc[s * n + i] + hr[s * n + i];
+            if (ctx->record_fn && flags[s] == kNoFail) {
+                std::vector<double> lo(n), hi(n);
+                for (uint64_t i = 0; i < n; ++i) {
+                    lo[i] = hc[s * n + i] - hr[s * n + i];
+                    hi[i] = hc[s * n + i] + hr[s * n + i];
+                }
+                ctx->record_fn(ctx->record_user, s, slot_steps[s], slot_times[s], lo.data(), hi.data(), n);
+            }
         }
     }
     return large_errors(ctx, method, p, plan.total, slot_steps, slot_times, hf[0], hf[1], flags, vals, n,

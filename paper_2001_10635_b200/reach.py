@@ -236,6 +236,26 @@ class Context:
     def lanes(self) -> int:
         return int(_lib.lib().pirk_lane_count(self._h))
 
+    def set_record_callback(self, fn) -> None:
+        """Stream recorded slots: ``fn(slot, step, t, lower, upper)`` (numpy
+        views valid during the call; copy to keep) once per slot, in order,
+        while the device integrates towards the next slot (pirk_c.h
+        pirk_set_record_callback; the StepObserver of rk4.hpp:63-64).  None
+        disables it.  With a callback the tube arrays may be skipped
+        (``out=(None, None)`` is not needed: pass ``keep_tube=False``)."""
+        if fn is None:
+            self._record = None
+            self.check(_lib.lib().pirk_set_record_callback(self._h, None, None))
+            return
+
+        def tramp(user, slot, step, t, lo, hi, n):
+            lo_a = np.ctypeslib.as_array(lo, shape=(n,))
+            hi_a = np.ctypeslib.as_array(hi, shape=(n,))
+            fn(int(slot), int(step), float(t), lo_a, hi_a)
+
+        self._record = _lib.RECORD_FN(tramp)  # keep the trampoline alive
+        self.check(_lib.lib().pirk_set_record_callback(self._h, C.cast(self._record, C.c_void_p), None))
+
     def release_cache(self) -> None:
         """Free the state buffers kept for the next run of the same size."""
         self.check(_lib.lib().pirk_release_cache(self._h))
