@@ -711,6 +711,8 @@ def main():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-exact", action="store_true")
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--launcher-check", action="store_true",
+                    help="print each rank's (rank, world) and exit: tests the --gpus relaunch without GPUs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -719,6 +721,11 @@ def main():
         relaunch_under_torchrun(args.gpus)
     if world and world != args.gpus:
         sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+    if args.launcher_check:
+        w, r, lr = dist_env()
+        print(json.dumps({"launcher_check": True, "rank": r, "local_rank": lr, "world": w,
+                          "n_gpus": args.gpus}), flush=True)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

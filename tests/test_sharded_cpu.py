@@ -165,3 +165,25 @@ def test_shard_geometry():
             assert lo <= s.begin and hi >= s.end
             covered.extend(range(s.begin, s.end))
         assert covered == list(range(units))
+
+
+def test_bench_gpus_flag_launches_n_ranks():
+    """`python bench.py --gpus 2` re-executes itself under torch.distributed.run
+    with two ranks (--gpus was parsed and ignored)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--launcher-check"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert sorted(l["rank"] for l in lines) == [0, 1]
+    assert all(l["world"] == 2 and l["n_gpus"] == 2 for l in lines)
+    # a WORLD_SIZE that disagrees with --gpus is refused
+    env2 = dict(env, WORLD_SIZE="3", RANK="0", LOCAL_RANK="0")
+    r2 = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--launcher-check"],
+                        cwd=root, env=env2, capture_output=True, text=True, timeout=120)
+    assert r2.returncode != 0 and "WORLD_SIZE=3" in r2.stderr
