@@ -76,6 +76,9 @@
 #if PIRK_STRIP_LADDER && !PIRK_STRIP_SPLITBAR
 #error "PIRK_STRIP_LADDER needs PIRK_STRIP_SPLITBAR"
 #endif
+#ifndef PIRK_STRIP_EDGECSE
+#define PIRK_STRIP_EDGECSE 1  // edge tiles of g % 4 == 0 grids: ghost values substituted per exchanged neighbour, shared pair sums
+#endif
 #ifndef PIRK_STRIP_SANITIZE
 // 1 (racecheck builds only): the halo warps' reads of the rows outside the
 // footprint (warp 0's row -1, warp 15's row 64) go to a private dummy row
@@ -126,8 +129,12 @@ __device__ __forceinline__ void heat_strip_report(const double* stp, int g, long
     }
 }
 
-template <bool Interior>
+// Kind: 0 interior tile, 1 edge tile of a g % 4 == 0 grid (PIRK_STRIP_EDGECSE),
+// 2 any other edge tile
+template <int Kind>
 struct HeatStrip {
+    static constexpr bool Interior = Kind == 0;
+    static constexpr bool EdgeCse = Kind == 1;
     const HeatStepParams& hp;
     double2* __restrict__ EX;  // exchange levels
     double* __restrict__ XR;   // x ring
@@ -220,6 +227,31 @@ struct HeatStrip {
         L[kSThreads + t] = make_double2(v[6], v[7]);
     }
 
+    // anti-diagonal pair sums P(r, c) = v(r, c+1) + v(r+1, c) are shared:
+    // point (r, 0) sums P(r, 0) + P(r-1, -1), point (r, 1) P(r, 1) + P(r-1, 0)
+    __device__ __forceinline__ static void cse_sums(const double (&C)[8], const double (&T)[2],
+                                                    const double (&B)[2], const double (&L)[4],
+                                                    const double (&R)[4], double (&s)[8]) {
+        auto V = [&](int r, int c) -> double {
+            if (r < 0) return T[c];
+            if (r > 3) return B[c];
+            if (c < 0) return L[r];
+            if (c > 1) return R[r];
+            return C[2 * r + c];
+        };
+        double pm = V(-1, 0) + V(0, -1);  // P(r-1, -1)
+        double p0 = V(-1, 1) + V(0, 0);   // P(r-1, 0)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const double q0 = V(r, 1) + V(r + 1, 0);  // P(r, 0)
+            const double q1 = V(r, 2) + V(r + 1, 1);  // P(r, 1)
+            s[2 * r] = q0 + pm;
+            s[2 * r + 1] = q1 + p0;
+            if (r < 3) pm = V(r, 0) + V(r + 1, -1);  // P(r, -1)
+            p0 = q0;
+        }
+    }
+
     // in-plane sums xm + xp + ym + yp of the 8 points of centre plane C
     __device__ __forceinline__ void inplane(const double (&C)[8], const double (&T)[2], const double (&B)[2],
                                             double (&s)[8]) const {
@@ -230,27 +262,30 @@ struct HeatStrip {
             R[r] = __shfl_down_sync(0xffffffffu, C[2 * r], 1);
         }
         if constexpr (Interior && PIRK_STRIP_CSE) {
-            // anti-diagonal pair sums P(r, c) = v(r, c+1) + v(r+1, c) are shared:
-            // point (r, 0) sums P(r, 0) + P(r-1, -1), point (r, 1) P(r, 1) + P(r-1, 0)
-            auto V = [&](int r, int c) -> double {
-                if (r < 0) return T[c];
-                if (r > 3) return B[c];
-                if (c < 0) return L[r];
-                if (c > 1) return R[r];
-                return C[2 * r + c];
-            };
-            double pm = V(-1, 0) + V(0, -1);  // P(r-1, -1)
-            double p0 = V(-1, 1) + V(0, 0);   // P(r-1, 0)
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const double q0 = V(r, 1) + V(r + 1, 0);  // P(r, 0)
-                const double q1 = V(r, 2) + V(r + 1, 1);  // P(r, 1)
-                s[2 * r] = q0 + pm;
-                s[2 * r + 1] = q1 + p0;
-                if (r < 3) pm = V(r, 0) + V(r + 1, -1);  // P(r, -1)
-                p0 = q0;
-            }
+            cse_sums(C, T, B, L, R, s);
             return;
+        }
+        if constexpr (EdgeCse) {
+            // g % 4 == 0: every grid face lies on a block edge -- x = 0 at a
+            // lane's column 0, x = g-1 at column 1, y = 0 at row 0, y = g-1 at
+            // row 3 -- so the ghost value of a face cell replaces exactly one
+            // exchanged neighbour (L, R, T or B), used by that cell alone:
+            // substitute it, then share pair sums as interior tiles do.
+            {
+                double L2[4], R2[4], T2[2], B2[2];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    L2[r] = (fx0 & 1) ? fma(-hp.robin, C[2 * r], C[2 * r + 1]) : L[r];  // Robin ghost
+                    R2[r] = (fxg & 2) ? C[2 * r + 1] : R[r];                             // insulated
+                }
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    T2[c] = (fy0 & 1) ? C[c] : T[c];
+                    B2[c] = (fyg & 8) ? C[6 + c] : B[c];
+                }
+                cse_sums(C, T2, B2, L2, R2, s);
+                return;
+            }
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
@@ -630,7 +665,13 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
         r.tt = tt;                                                                                   \
         r.run();                                                                                     \
     }
-    if (interior) PIRK_STRIP_RUN(true) else PIRK_STRIP_RUN(false)
+#ifdef PIRK_STRIP_TIMING_ONLY_INTERIOR  // A/B timing only: every tile runs the interior code (wrong at edges)
+    if (true) PIRK_STRIP_RUN(0)
+#else
+    if (interior) PIRK_STRIP_RUN(0)
+#endif
+    else if (PIRK_STRIP_EDGECSE && g % 4 == 0) PIRK_STRIP_RUN(1)
+    else PIRK_STRIP_RUN(2)
 #undef PIRK_STRIP_RUN
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
     tmem_fence_before();
