@@ -117,6 +117,23 @@ def heat_kernel_name(mode, grid):
     return "heat2_step_kernel"
 
 
+def allreduce(dist, t, op):
+    """All-reduce a device tensor in place (through the host on gloo, which
+    the one-GPU multi-rank test of the N > 1 path uses)."""
+    if dist.get_backend() == "gloo":
+        c = t.cpu()
+        dist.all_reduce(c, op=op)
+        t.copy_(c)
+    else:
+        dist.all_reduce(t, op=op)
+
+
+def device_of(args, local):
+    """cuda device of a rank: its LOCAL_RANK, or 0 for --same-device (testing
+    the N > 1 code path with several ranks on one GPU)."""
+    return 0 if args.same_device else local
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -131,6 +148,7 @@ def heat_device_bench(args, world, rank, local, torch, pk, dist):
     from paper_2001_10635_b200 import sharded as S
 
     model = pk.make_heat3d(args.grid)
+    local = device_of(args, local)
     ctx = pk.Context(local, args.mode)
     K = 1
     shard = S.Shard(args.grid, world, rank, 4 * K)
@@ -170,7 +188,7 @@ def heat_device_bench(args, world, rank, local, torch, pk, dist):
     ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        allreduce(dist, t, dist.ReduceOp.MAX)
     ms_max = float(t.item())
     run.check(0.0, args.h)  # raises the reference's IntegrationError on any rank's failure
     check = state_check(run, args, torch, dist, world)
@@ -208,7 +226,7 @@ def state_check(run, args, torch, dist, world):
     # the first row of every rank is the same physical line: compare rank 0's
     v = torch.stack([ok.to(torch.float64), -worst])
     if world > 1:
-        dist.all_reduce(v, op=dist.ReduceOp.MIN)
+        allreduce(dist, v, dist.ReduceOp.MIN)
     return {"finite_ordered_bounded": bool(v[0].item() == 1.0),
             "plane_invariance_max_rel": float(-v[1].item()),
             "plane_invariance_ok": float(-v[1].item()) <= (0.0 if args.mode == "exact" else 1e-12)}
@@ -288,6 +306,7 @@ def heat_e2e_sharded(args, pk, torch, dist, world, rank, local):
     g = args.grid
     unit = g * g
     model = pk.make_heat3d(g)
+    local = device_of(args, local)
     ctx = pk.Context(local, args.mode)
     shard = S.Shard(g, world, rank, 4)
     dev = torch.device("cuda", local)
@@ -324,7 +343,7 @@ def heat_e2e_sharded(args, pk, torch, dist, world, rank, local):
     bad = once()
     dt = time.perf_counter() - t0
     tt = torch.tensor([dt, float(bad)], dtype=torch.float64, device=dev)
-    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    allreduce(dist, tt, dist.ReduceOp.MAX)
     n = g ** 3
     res = {"value": 2.0 * n * len(steps) / tt[0].item(), "unit": UNIT,
            "h2d_bytes_per_step": 2 * 8 * (n + 2 * (world - 1) * 4 * unit), "d2h_bytes_per_step": 2 * n * 8,
@@ -514,8 +533,9 @@ def sharded_chain_bench(args, world, rank, local, torch, pk, dist):
     reach timed on the device, max over ranks."""
     from paper_2001_10635_b200 import sharded as S
 
-    n, K, steps = 10 ** 7, 8, 100
+    n, K, steps = args.chain_n, 8, 100
     model = pk.make_chain(n)
+    local = device_of(args, local)
     ctx = pk.Context(local, args.mode)
     shard = S.Shard(n, world, rank, 4 * K)
     run = S.ShardedReach(model, "mixed-monotonicity", shard, S.device_step_fn(model, "mixed-monotonicity", ctx),
@@ -542,7 +562,7 @@ def sharded_chain_bench(args, world, rank, local, torch, pk, dist):
     run.check(0.0, 0.01)
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        allreduce(dist, t, dist.ReduceOp.MAX)
     ms = float(t.item())
     del a, run
     torch.cuda.empty_cache()
@@ -550,7 +570,8 @@ def sharded_chain_bench(args, world, rank, local, torch, pk, dist):
     timed = steps - K
     return {"value": 2.0 * n * timed / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / timed,
             "n_gpus": world, "halo_units": 4 * K, "steps_per_exchange": K,
-            "workload": "C4 coupled chain n=1e7 CTMM, index-range shards, NCCL halos, 92 timed steps",
+            "workload": f"C4 coupled chain n={n} CTMM, index-range shards, {dist.get_backend() if world > 1 else 'no'} halos, "
+                        f"{timed} timed steps",
             "scaling": "strong"}
 
 
@@ -562,8 +583,11 @@ def run_ours(args):
 
     world, rank, local = dist_env()
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device_of(args, local)))
+        else:
+            dist.init_process_group("gloo")
+    torch.cuda.set_device(device_of(args, local))
     pk.set_default_mode(args.mode)
     ms, launches, clocks, check, _ = heat_device_bench(args, world, rank, local, torch, pk, dist)
     n = args.grid ** 3
@@ -711,6 +735,11 @@ def main():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-exact", action="store_true")
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process group backend for N > 1 (gloo: testing only, halos staged through the host)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="every rank on cuda:0 (tests the N > 1 code path on one GPU; with --backend gloo)")
+    ap.add_argument("--chain-n", type=int, default=10 ** 7)
     ap.add_argument("--launcher-check", action="store_true",
                     help="print each rank's (rank, world) and exit: tests the --gpus relaunch without GPUs")
     args = ap.parse_args()

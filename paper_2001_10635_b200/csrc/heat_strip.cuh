@@ -332,6 +332,7 @@ struct HeatStrip {
         const bool a4 = !edge || (v3 && j - 3 >= ob && j - 3 < oe);  // A4(j-3) needed next iteration
         const bool has_x = !edge || j < ze;
 
+        if constexpr (!PIRK_TM_LD_WAITST) tm_wait_st();  // the previous plane's TMEM stores land before its slots are read
         // ---- x(j): wait for its box; prefetch x(j+2) into the slot of x(j-2)
         const double* Xj = xslot(xs);
         const double* Xm = xslot((xs + 3) & 3);  // x(j-1)

@@ -101,6 +101,11 @@ class HaloExchanger:
         """fields: list of 1-D tensors of length win_len*unit (window layout)."""
         self.finish(self.start(fields))
 
+    def _staged(self) -> bool:
+        """gloo cannot move CUDA tensors point-to-point: halos then go through
+        host copies (multi-rank tests on one GPU; NCCL moves device memory)."""
+        return self.dist.get_backend(self.group) == "gloo"
+
     def start(self, fields):
         """Post the halo sends / receives and return a handle for finish().  The
         sends read the owned boundary units in place and the receives land
@@ -112,25 +117,34 @@ class HaloExchanger:
         H = s.halo
         u = self.unit
         ops = []
+        staged = []
         left, right = s.rank - 1, s.rank + 1
         wb = s.win_begin
+        stage = self._staged()
+
+        def post(snd, rcv, peer):
+            if stage and snd.is_cuda:
+                snd, dev_rcv = snd.cpu(), rcv
+                rcv = dev_rcv.new_empty(dev_rcv.shape, device="cpu")
+                staged.append((dev_rcv, rcv))
+            ops.append(self.dist.P2POp(self.dist.isend, snd, peer, self.group))
+            ops.append(self.dist.P2POp(self.dist.irecv, rcv, peer, self.group))
+
         for f in fields:
             if left >= 0:
-                snd = f[(s.begin - wb) * u:(s.begin - wb + H) * u]
-                rcv = f[0:(s.begin - wb) * u]
-                ops.append(self.dist.P2POp(self.dist.isend, snd, left, self.group))
-                ops.append(self.dist.P2POp(self.dist.irecv, rcv, left, self.group))
+                post(f[(s.begin - wb) * u:(s.begin - wb + H) * u], f[0:(s.begin - wb) * u], left)
             if right < s.world:
-                snd = f[(s.end - wb - H) * u:(s.end - wb) * u]
-                rcv = f[(s.end - wb) * u:(s.win_end - wb) * u]
-                ops.append(self.dist.P2POp(self.dist.isend, snd, right, self.group))
-                ops.append(self.dist.P2POp(self.dist.irecv, rcv, right, self.group))
-        return self.dist.batch_isend_irecv(ops) if ops else []
+                post(f[(s.end - wb - H) * u:(s.end - wb) * u], f[(s.end - wb) * u:(s.win_end - wb) * u], right)
+        return (self.dist.batch_isend_irecv(ops) if ops else []), staged
 
     def finish(self, handle):
-        """Wait for the exchange (the halos are already in place)."""
-        for r in handle:
+        """Wait for the exchange (the halos are already in place, or copied in
+        from the host staging buffers on gloo)."""
+        reqs, staged = handle
+        for r in reqs:
             r.wait()
+        for dev, host in staged:
+            dev.copy_(host)
 
 
 def device_step_fn(model: SystemModel, method: str, ctx=None):
@@ -226,6 +240,8 @@ class ShardedReach:
         v = torch.where(v == -1, torch.full_like(v, big), v)  # no failure -> +inf
         import torch.distributed as dist
         if self.shard.world > 1 and dist.is_available() and dist.is_initialized():
+            if dist.get_backend(group) == "gloo":
+                v = v.cpu()
             dist.all_reduce(v, op=dist.ReduceOp.MIN, group=group)
         keys = [NO_FAIL if int(x) == big else int(x) for x in v.cpu().tolist()]
         msg = failure_message(self.method, keys, t0, h)
