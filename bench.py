@@ -727,8 +727,8 @@ def main():
     ap.add_argument("--grid", type=int, default=GRID)
     ap.add_argument("--h", type=float, default=H)
     ap.add_argument("--cpu-grid", type=int, default=300)
-    ap.add_argument("--cpu-grid-max", type=int, default=1000)
-    ap.add_argument("--cpu-steps", type=int, default=1)
+    ap.add_argument("--cpu-grid-max", type=int, default=800)
+    ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--ref-steps-per-call", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
