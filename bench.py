@@ -311,10 +311,15 @@ def heat_e2e_sharded(args, pk, torch, dist, world, rank, local):
     shard = S.Shard(g, world, rank, 4)
     dev = torch.device("cuda", local)
     win, own = shard.win_len * unit, (shard.end - shard.begin) * unit
-    h_lo = torch.full((win,), 0.9, dtype=torch.float64).pin_memory()
-    h_hi = torch.full((win,), 1.1, dtype=torch.float64).pin_memory()
-    o_lo = torch.empty((own,), dtype=torch.float64).pin_memory()
-    o_hi = torch.empty((own,), dtype=torch.float64).pin_memory()
+    # page-locked through cudaHostRegister (torch's pinned allocator rounds up to
+    # powers of two: 8 ranks x 4 x 8 GB would not fit a host)
+    host = [np.empty(win), np.empty(win), np.empty(own), np.empty(own)]
+    cudart = torch.cuda.cudart()
+    for b in host:
+        cudart.cudaHostRegister(b.ctypes.data, b.nbytes, 0)
+    host[0].fill(0.9)
+    host[1].fill(1.1)
+    h_lo, h_hi, o_lo, o_hi = (torch.from_numpy(b) for b in host)
     run = S.ShardedReach(model, "mixed-monotonicity", shard, S.device_step_fn(model, "mixed-monotonicity", ctx),
                          S.HaloExchanger(shard, unit), K=1)
     steps = S.plan_rk4_steps(0.0, C5_STEPS * args.h, args.h)
@@ -350,7 +355,9 @@ def heat_e2e_sharded(args, pk, torch, dist, world, rank, local):
            "seconds": tt[0].item(), "rk4_steps": len(steps), "n": n, "grid": g,
            "api": "paper_2001_10635_b200.sharded.ShardedReach (one process per GPU, NCCL halos)",
            "order_violated": bool(tt[1].item()), "timing": "wall clock of the whole call, max over ranks"}
-    del a, run
+    del a, run, h_lo, h_hi, o_lo, o_hi
+    for b in host:
+        cudart.cudaHostUnregister(b.ctypes.data)
     torch.cuda.empty_cache()
     ctx.close()
     return res
@@ -503,6 +510,29 @@ def secondary(args, pk, torch):
                               "cores": threads, "kind": "reference",
                               "sample": "ivreach::mixed_monotonicity chain n=1e7, first 10 of the 100 steps"}
     out["C4_chain_sdmm_n1e7"] = c4
+    # C1: CTMM of the 12-state arch-quadrotor (Jacobian-bound decomposition,
+    # SURVEY.md 8d), 100 steps, stride 10: one small embedding integrated by one
+    # device thread -- latency-bound; reported with the reference beside it
+    mq = pk.with_jacobian_decomposition(pk.make_arch_quadrotor())
+    lo = np.array([-0.4] * 6 + [0.0] * 6)
+    p = pk.ReachProblem(mq, pk.IntervalVector(lo, -lo), None, 0.0, 1.0, 0.01, 10)
+    pk.mixed_monotonicity(p, ctx=ctx)
+    reps = 20
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        tube = pk.mixed_monotonicity(p, ctx=ctx)
+    dt = (time.perf_counter() - t0) / reps
+    c1 = {"value": 24.0 * tube.report.steps / dt, "unit": UNIT, "call_ms": dt * 1e3,
+          "kernel_ms": tube.report.phases.integration_s * 1e3,
+          "bound": "latency: one device thread integrates the 24-dimensional embedding (RK4 stages are "
+                   "sequential); a single small problem does not fill a GPU"}
+    if ref_ok:
+        r1 = O.ref_reach(O.METHOD_MM, mq, lo, -lo, None, None, 0.0, 1.0, 0.01, 10, workers=1, keep=False)
+        c1["cpu_baseline"] = {"value": 24.0 * r1.report["steps"] / r1.report["integration_s"], "unit": UNIT,
+                              "cores": 1, "kind": "reference",
+                              "sample": "ivreach::mixed_monotonicity arch-quadrotor (Jacobian decomposition), "
+                                        "the full C1 reach on one worker"}
+    out["C1_archquad_ctmm_n12"] = c1
     # C2: arch-quadrotor Monte Carlo, m = 1e6, 100 steps: FP64-bound
     mq = pk.make_arch_quadrotor()
     lo = np.array([-0.4] * 6 + [0.0] * 6)

@@ -85,6 +85,7 @@ struct pirk_ctx {
     // size: freeing 4 x 32 GB costs up to ~0.5 s of unmapping per call
     std::vector<CachedBlock> cache;
     std::vector<PirkLane> peers;  // lanes 1 .. W-1 (empty for a one-device context)
+    bool peer_stores = true;      // every adjacent pair of lanes can address the other's memory
     // streaming observer (pirk_set_record_callback): called per recorded slot
     pirk_record_fn record_fn = nullptr;
     void* record_user = nullptr;
@@ -1129,10 +1130,25 @@ pirk_status run_large_multi(pirk_ctx* ctx, const pirk_model* m, int method, cons
     const double setup_s = since(t_setup);
     const auto t_int = Clock::now();
     const bool ex = exact_mode(ctx);
-    auto launch = [&](ShardState& z, const StepConsts& sc, uint64_t k, uint64_t ob, uint64_t oe) -> cudaError_t {
+    // Halo transfer: the boundary launch itself stores its units into the
+    // neighbour's halo over NVLink peer memory (WindowArgs::mir0/1) -- one
+    // kernel computes and sends; PIRK_LANE_HALO=copy (or lanes without peer
+    // access) sends them with cudaMemcpyPeerAsync on the copy stream instead.
+    static const bool halo_copy_env = [] {
+        const char* v = std::getenv("PIRK_LANE_HALO");
+        return v && std::strcmp(v, "copy") == 0;
+    }();
+    const bool fused = ctx->peer_stores && !halo_copy_env;
+    auto launch = [&](ShardState& z, const StepConsts& sc, uint64_t k, uint64_t ob, uint64_t oe,
+                      ShardState* mirror = nullptr) -> cudaError_t {
         if (ob >= oe) return cudaSuccess;
         const size_t off = (ob - z.wb) * unit;
         WindowArgs w{z.in0(), z.in1(), z.out0() + off, z.out1() + off, z.wb, z.we, ob, oe};
+        if (mirror) {  // unit ob at the same place of the neighbour's output window
+            const size_t moff = (ob - mirror->wb) * unit;
+            w.mir0 = mirror->out0() + moff;
+            w.mir1 = mirror->out1() + moff;
+        }
         ctx->launches++;
         if (is_chain(m))
             return ex ? launch_chain_step<true>(cm, w, sc, k, z.fail.p, z.L.s)
@@ -1157,10 +1173,14 @@ pirk_status run_large_multi(pirk_ctx* ctx, const pirk_model* m, int method, cons
                     if (right) CK(ctx, cudaStreamWaitEvent(z.L.s, sh[static_cast<size_t>(r + 1)].sent[(k - 1) & 1], 0));
                 }
                 // 1. boundary units, the ones the neighbours read next step
-                if (left) CK(ctx, launch(z, sc, k, z.b, z.b + 4));
-                if (right) CK(ctx, launch(z, sc, k, z.e - 4, z.e));
-                // 2. their peer copies, on the copy stream
-                if (left || right) {
+                //    (fused: written into the neighbours' halos by the same launch)
+                ShardState* yl = left ? &sh[static_cast<size_t>(r - 1)] : nullptr;
+                ShardState* yr = right ? &sh[static_cast<size_t>(r + 1)] : nullptr;
+                if (left) CK(ctx, launch(z, sc, k, z.b, z.b + 4, fused ? yl : nullptr));
+                if (right) CK(ctx, launch(z, sc, k, z.e - 4, z.e, fused ? yr : nullptr));
+                if (fused && (left || right)) CK(ctx, cudaEventRecord(z.sent[k & 1], z.L.s));
+                // 2. else their peer copies, on the copy stream
+                if (!fused && (left || right)) {
                     CK(ctx, cudaEventRecord(z.bnd, z.L.s));
                     CK(ctx, cudaStreamWaitEvent(z.L.xs, z.bnd, 0));
                     if (left) {
@@ -1653,6 +1673,12 @@ pirk_status pirk_create_multi(int n_lanes, const int* devices, pirk_ctx** out) {
                 cudaSetDevice(from);
                 const cudaError_t pe = cudaDeviceEnablePeerAccess(to, 0);
                 if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else if (pe != cudaSuccess) {
+                    cudaGetLastError();
+                    ctx->peer_stores = false;
+                }
+            } else {
+                ctx->peer_stores = false;  // halos then move by copy engine (staged by the driver)
             }
         }
     }

@@ -250,7 +250,7 @@ struct HeatCols {
     int wd;
 };
 
-template <bool Exact, bool Interior, bool Tma>
+template <bool Exact, bool Interior, bool Tma, bool Mirror = false>
 struct HeatRun {
     const HeatStepParams& hp;
     const StepConsts& sc;
@@ -268,6 +268,7 @@ struct HeatRun {
     const void* tmap;
     int bx0, by0, wbz;
     unsigned long long* bars;
+    double* mdst;  // Mirror: the neighbour lane's halo planes (WindowArgs::mir0/1), indexed like dst
 
     // register state: slot (p - zs) & 3 of plane p
     double ox[2][4], ou1[2][4], ou2[2][4], ou3[2][4];
@@ -286,6 +287,7 @@ struct HeatRun {
     // running plane pointers: x-plane j+1 (loads) and output plane j-4 (stores)
     const double* ldp;
     double* stp;
+    double* mtp;  // Mirror: stp in the neighbour's window
 
     // x-plane p -> x-ring slot s.  TMA: one thread issues the whole 40x40 box
     // (out-of-grid cells zero-filled), completion on bars[s].  Fallback: each
@@ -494,7 +496,10 @@ struct HeatRun {
                 for (int k = 0; k < 2; ++k) {
                     xn[k] = Exact ? xs[k] + sc.h6 * (acc[k] + kk[k])
                                   : fma(hp.h6kk, acc[k] + kk[k], xs[k]);
-                    if (in(k)) out[c.og + k] = xn[k];
+                    if (in(k)) {
+                        out[c.og + k] = xn[k];
+                        if constexpr (Mirror) mtp[c.og + k] = xn[k];
+                    }
                 }
                 // one test per pair: the sum is non-finite whenever either value
                 // is (a finite overflow only sends the pair to the exact check)
@@ -523,6 +528,7 @@ struct HeatRun {
         }
         ldp += g2;
         stp += g2;
+        if constexpr (Mirror) mtp += g2;
         if constexpr (!Tma) cp_async_wait_all();  // x(j+1) landed (own copies); barrier publishes it
         __syncthreads();
     }
@@ -549,6 +555,7 @@ struct HeatRun {
         __syncthreads();
         ldp = src + static_cast<long long>(zs + 1) * g2;
         stp = dst + static_cast<long long>(zs - 4) * g2;
+        if constexpr (Mirror) mtp = mdst + static_cast<long long>(zs - 4) * g2;
         const int jend = ze + kHeatH;
         // Steady-state iterations: all four stages valid and planes j-5 .. j
         // clear of the insulated z faces, so the unrolled main loop carries no
@@ -580,7 +587,7 @@ struct HeatTmaps {
     CUtensorMap f[2];
 };
 
-template <bool Exact>
+template <bool Exact, bool Mirror = false>
 __global__ void __launch_bounds__(kHeatThreads, 1)
 heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
                  const StepConsts sc, const unsigned long long step, const uint64_t zchunk,
@@ -677,12 +684,13 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
     const void* tmap = &tm.f[field];
     const int bx0 = static_cast<int>(ix0) - kHeatH, by0 = static_cast<int>(iy0) - kHeatH;
     const int wbz = static_cast<int>(w.win_begin);
+    double* mdst = Mirror ? (field ? w.mir1 : w.mir0) - static_cast<long long>(w.out_begin) * g2 : nullptr;
 #define PIRK_HEAT_RUN(INTERIOR, TMA)                                                               \
     {                                                                                              \
-        HeatRun<Exact, INTERIOR, TMA> r{hp, sc, c, smem, zs, ze, static_cast<int>(obz),           \
+        HeatRun<Exact, INTERIOR, TMA, Mirror> r{hp, sc, c, smem, zs, ze, static_cast<int>(obz),   \
                                         static_cast<int>(oez), static_cast<int>(g), zs > 0, ze < g, \
                                         g2, src, dst, field, m.method, step, fail, n_total, tmap,  \
-                                        bx0, by0, wbz, bars};                                      \
+                                        bx0, by0, wbz, bars, mdst};                                \
         r.tacc = tacc;                                                                             \
         r.run();                                                                                   \
     }

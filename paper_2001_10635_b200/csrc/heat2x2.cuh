@@ -88,7 +88,7 @@ struct Heat2Cols {
     int wd[2];     // warp-uniform max depth of ring slots 0 and 1
 };
 
-template <bool Exact, bool Interior, bool Tma>
+template <bool Exact, bool Interior, bool Tma, bool Mirror = false>
 struct Heat2Run {
     const HeatStepParams& hp;
     const StepConsts& sc;
@@ -105,6 +105,7 @@ struct Heat2Run {
     const void* tmap;
     int bx0, by0, wbz;
     unsigned long long* bars;
+    double* mdst;  // Mirror: the neighbour lane's halo planes, indexed like dst
 
     // own block: [point k][plane slot (p - zs) & 3]
     double ox[4][4], ou1[4][4], ou2[4][4], ou3[4][4];
@@ -115,6 +116,7 @@ struct Heat2Run {
     bool vec;  // outputs 16-byte aligned at even offsets (g even, aligned windows)
     const double* ldp;
     double* stp;
+    double* mtp;  // Mirror: stp in the neighbour's window
 
     __device__ __forceinline__ bool in(int k) const { return Interior || (c.of[k] & kIn); }
     __device__ __forceinline__ int goff(int k) const { return c.og + (k & 1) + (k >> 1) * g; }
@@ -378,6 +380,11 @@ struct Heat2Run {
                     for (int k = 0; k < 4; ++k)
                         if (in(k)) out[(k & 1) + (k >> 1) * g] = xn[k];
                 }
+                if constexpr (Mirror) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (in(k)) mtp[c.og + (k & 1) + (k >> 1) * g] = xn[k];
+                }
                 if (!finite_d((xn[0] + xn[1]) + (xn[2] + xn[3]))) {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
@@ -406,6 +413,7 @@ struct Heat2Run {
         }
         ldp += g2;
         stp += g2;
+        if constexpr (Mirror) mtp += g2;
         if constexpr (!Tma) cp_async_wait_all();
         __syncthreads();
     }
@@ -432,6 +440,7 @@ struct Heat2Run {
         __syncthreads();
         ldp = src + static_cast<long long>(zs + 1) * g2;
         stp = dst + static_cast<long long>(zs - 4) * g2;
+        if constexpr (Mirror) mtp = mdst + static_cast<long long>(zs - 4) * g2;
         const int jend = ze + kHeatH;
         // steady-state bounds: as HeatRun::run
         int a = zs + 3 + 3 * lo_shift;
@@ -455,7 +464,7 @@ struct Heat2Run {
     }
 };
 
-template <bool Exact>
+template <bool Exact, bool Mirror = false>
 __global__ void __launch_bounds__(kHeat2Threads, 1)
 heat2_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
                   const StepConsts sc, const unsigned long long step, const uint64_t zchunk,
@@ -549,12 +558,13 @@ heat2_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
     const void* tmap = &tm.f[field];
     const int bx0 = static_cast<int>(ix0) - kHeatH, by0 = static_cast<int>(iy0) - kHeatH;
     const int wbz = static_cast<int>(w.win_begin);
+    double* mdst = Mirror ? (field ? w.mir1 : w.mir0) - static_cast<long long>(w.out_begin) * g2 : nullptr;
 #define PIRK_HEAT2_RUN(INTERIOR, TMA)                                                              \
     {                                                                                              \
-        Heat2Run<Exact, INTERIOR, TMA> r{hp, sc, c, smem, zs, ze, static_cast<int>(obz),          \
+        Heat2Run<Exact, INTERIOR, TMA, Mirror> r{hp, sc, c, smem, zs, ze, static_cast<int>(obz),  \
                                          static_cast<int>(oez), static_cast<int>(g), zs > 0,      \
                                          ze < g, g2, src, dst, field, m.method, step, fail,        \
-                                         n_total, tmap, bx0, by0, wbz, bars};                      \
+                                         n_total, tmap, bx0, by0, wbz, bars, mdst};                \
         r.tacc = tacc;                                                                             \
         r.vec = (flags & 2) != 0;                                                                  \
         r.run();                                                                                   \
@@ -629,7 +639,13 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(kHeatSmemBytes));
         if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(heat_step_kernel<Exact, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kHeatSmemBytes));
+        if (e == cudaSuccess)
             e = cudaFuncSetAttribute(heat2_step_kernel<Exact>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kHeatSmemBytes));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(heat2_step_kernel<Exact, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(kHeatSmemBytes));
         if constexpr (!Exact) {
 #if PIRK_DEV_VARIANTS
@@ -642,6 +658,9 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSSmemBytes));
             if (e == cudaSuccess)
                 e = cudaFuncSetAttribute(heat_strip_kernel<Exact, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSSmemBytes));
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(heat_strip_kernel<Exact, false, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSSmemBytes));
         }
         if (e != cudaSuccess) return e;
@@ -679,6 +698,9 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
             if (field_only >= 0)
                 heat_strip_kernel<Exact, true><<<grid, kSThreads, kSSmemBytes, stream>>>(
                     m, hp, w, sc, step, zchunk, fail, tm, 1 | (vec ? 2 : 0) | fsel);
+            else if (w.mir0)
+                heat_strip_kernel<Exact, false, true><<<grid, kSThreads, kSSmemBytes, stream>>>(
+                    m, hp, w, sc, step, zchunk, fail, tm, 1 | (vec ? 2 : 0));
             else
                 heat_strip_kernel<Exact, false><<<grid, kSThreads, kSSmemBytes, stream>>>(
                     m, hp, w, sc, step, zchunk, fail, tm, 1 | (vec ? 2 : 0));
@@ -710,8 +732,15 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
     const int tma = heat_encode_tmap(&tm.f[0], w.in0, m.g, wplanes) &&
                     heat_encode_tmap(&tm.f[1], w.in1, m.g, wplanes);
     if (variant >= 1) {
-        heat2_step_kernel<Exact><<<grid, kHeat2Threads, kHeatSmemBytes, stream>>>(
-            m, hp, w, sc, step, zchunk, fail, tm, tma | (vec ? 2 : 0));
+        if (w.mir0)
+            heat2_step_kernel<Exact, true><<<grid, kHeat2Threads, kHeatSmemBytes, stream>>>(
+                m, hp, w, sc, step, zchunk, fail, tm, tma | (vec ? 2 : 0));
+        else
+            heat2_step_kernel<Exact><<<grid, kHeat2Threads, kHeatSmemBytes, stream>>>(
+                m, hp, w, sc, step, zchunk, fail, tm, tma | (vec ? 2 : 0));
+    } else if (w.mir0) {
+        heat_step_kernel<Exact, true><<<grid, kHeatThreads, kHeatSmemBytes, stream>>>(m, hp, w, sc, step, zchunk,
+                                                                                      fail, tm, tma);
     } else {
         heat_step_kernel<Exact><<<grid, kHeatThreads, kHeatSmemBytes, stream>>>(m, hp, w, sc, step, zchunk,
                                                                                 fail, tm, tma);

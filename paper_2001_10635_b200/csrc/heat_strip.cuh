@@ -131,7 +131,7 @@ __device__ __forceinline__ void heat_strip_report(const double* stp, int g, long
 
 // Kind: 0 interior tile, 1 edge tile of a g % 4 == 0 grid (PIRK_STRIP_EDGECSE),
 // 2 any other edge tile
-template <int Kind>
+template <int Kind, bool Mirror = false>
 struct HeatStrip {
     static constexpr bool Interior = Kind == 0;
     static constexpr bool EdgeCse = Kind == 1;
@@ -144,6 +144,7 @@ struct HeatStrip {
     int zs, ze, ob, oe, g, lo_shift, hi_shift;
     long long g2;
     double* __restrict__ stp;  // output plane j-4 at the own block's (0,0)
+    double* mtp;               // Mirror: stp in the neighbour lane's window
     bool st_own;               // own block with all 8 cells in the grid (vector stores)
     unsigned st_mask;          // edge tiles: per-cell store mask (bit 2r+c)
     int gout;                  // in-plane global offset of the block's (0,0) cell
@@ -505,6 +506,12 @@ struct HeatStrip {
                     for (int i = 0; i < 8; ++i)
                         if ((st_mask >> i) & 1) stp[(i >> 1) * g + (i & 1)] = y[i];
                 }
+                if constexpr (Mirror) {  // the same cells into the neighbour's halo, over peer memory
+                    const unsigned mk = st_own ? 0xffu : st_mask;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        if ((mk >> i) & 1) mtp[(i >> 1) * g + (i & 1)] = y[i];
+                }
                 if ((st_own || st_mask) &&
                     !finite_d(((y[0] + y[1]) + (y[2] + y[3])) + ((y[4] + y[5]) + (y[6] + y[7]))))
                     heat_strip_report(stp, g, g2, j - 4, gout, st_own ? 0xffu : st_mask, field, method, step,
@@ -527,6 +534,7 @@ struct HeatStrip {
             xs = (xs + 1) & 3;
         }
         stp += g2;
+        if constexpr (Mirror) mtp += g2;
         // one barrier per plane: this iteration's rows (buffer j & 1) become
         // readable, and the next iteration may overwrite buffer (j - 1) & 1
         if constexpr (PIRK_STRIP_SPLITBAR) {
@@ -571,7 +579,7 @@ struct HeatStrip {
     }
 };
 
-template <bool Exact, bool One = false>
+template <bool Exact, bool One = false, bool Mirror = false>
 __global__ void __launch_bounds__(kSThreads, 1)
 heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w, const StepConsts sc,
                   const unsigned long long step, const uint64_t zchunk,
@@ -626,6 +634,7 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
     const int zs = static_cast<int>((obz - kHeatH > 0) ? obz - kHeatH : 0);
     const int ze = static_cast<int>((oez + kHeatH < g) ? oez + kHeatH : g);
     double* dst = (field ? w.out1 : w.out0) - static_cast<long long>(w.out_begin) * g2;
+    double* mdst = Mirror ? (field ? w.mir1 : w.mir0) - static_cast<long long>(w.out_begin) * g2 : nullptr;
 
     if (warp == 0) tmem_alloc512(&tmem_base);
     if (tid == 0) {
@@ -643,7 +652,7 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
                                                           static_cast<unsigned>(128 * (warp >> 2)));
 #define PIRK_STRIP_RUN(INTERIOR)                                                                     \
     {                                                                                                \
-        HeatStrip<INTERIOR> r{hp};                                                                   \
+        HeatStrip<INTERIOR, Mirror> r{hp};                                                           \
         r.EX = reinterpret_cast<double2*>(smem);                                                     \
         r.XR = smem + kSEdgeBytes / sizeof(double);                                                  \
         r.t = tid;                                                                                   \
@@ -654,6 +663,7 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
         r.g2 = g2;                                                                                   \
         r.gout = gout;                                                                               \
         r.stp = dst + static_cast<long long>(zs - 4) * g2 + gout;                                    \
+        if constexpr (Mirror) r.mtp = mdst + static_cast<long long>(zs - 4) * g2 + gout;             \
         r.st_own = st_own, r.st_mask = st_mask;                                                      \
         r.fx0 = fx0, r.fxg = fxg, r.fy0 = fy0, r.fyg = fyg;                                          \
         r.field = field, r.method = m.method, r.step = step, r.fail = fail;                          \

@@ -18,6 +18,11 @@ struct WindowArgs {
     double* out1;
     uint64_t win_begin, win_end;
     uint64_t out_begin, out_end;
+    // mirror outputs (or null): every value stored to out0[k] / out1[k] is also
+    // stored to mir0[k] / mir1[k] -- a neighbour lane's halo over NVLink peer
+    // memory, written by the kernel that computes it (engine.cu run_large_multi)
+    double* mir0 = nullptr;
+    double* mir1 = nullptr;
 };
 
 // 1-D radius-1 models on two fields (traffic MM/GB, coupled chain MM).

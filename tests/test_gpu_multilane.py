@@ -1,9 +1,10 @@
 """Multi-lane contexts (pirk_create_multi): the C-ABI's own multi-GPU path.
 
 On a one-GPU box every lane maps to cuda:0 (a repeated device id), which runs
-the identical code -- per-lane windows, boundary-first launches, halo peer
-copies (device-local here, NVLink between distinct GPUs), double-buffered
-cross-lane events, per-lane Monte Carlo ranges folded exactly.  Every result
+the identical code -- per-lane windows, boundary-first launches that store
+their units into the neighbours' halos (device-local here, NVLink peer memory
+between distinct GPUs; or copy-engine copies with PIRK_LANE_HALO=copy),
+double-buffered cross-lane events, per-lane Monte Carlo ranges folded exactly.  Every result
 must be bit-identical to the one-lane run and to the oracle.
 """
 import numpy as np
@@ -220,3 +221,19 @@ def test_release_cache_frees_state():
         assert free1 - free0 >= 4 * 2_000_000 * 8 * 0.9
     finally:
         ctx.close()
+
+
+def test_copy_engine_halo_path():
+    """PIRK_LANE_HALO=copy: halos by cudaMemcpyPeerAsync on the copy stream
+    instead of the fused peer stores of the boundary launches (the fallback
+    for lanes without peer access) -- same bit-identical results.  The env
+    var is read once per process, so the lane tests rerun in a child."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PIRK_LANE_HALO="copy")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        os.path.join(root, "tests", "test_gpu_multilane.py"), "-k", "lanes and not copy"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
