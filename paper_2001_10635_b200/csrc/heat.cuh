@@ -695,7 +695,11 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
         r.run();                                                                                   \
     }
     if (tma) {
+#ifdef PIRK_HEAT_TIMING_ONLY_INTERIOR  // A/B timing only (wrong at edge tiles)
+        PIRK_HEAT_RUN(true, true)
+#else
         if (interior) PIRK_HEAT_RUN(true, true) else PIRK_HEAT_RUN(false, true)
+#endif
     } else {
         if (interior) PIRK_HEAT_RUN(true, false) else PIRK_HEAT_RUN(false, false)
     }
