@@ -605,6 +605,50 @@ def sharded_chain_bench(args, world, rank, local, torch, pk, dist):
             "scaling": "strong"}
 
 
+def sharded_mc_bench(args, world, rank, local, torch, pk, dist):
+    """BASELINE config 2 at N GPUs: arch-quadrotor Monte Carlo, m = 1e6 samples
+    split into per-rank index ranges (counter-based draws: no communication),
+    each rank folding its hull (pirk_monte_carlo_range), then one MIN and one
+    MAX all-reduce of the hull; wall time of the whole call
+    including the reduction, max over ranks."""
+    from paper_2001_10635_b200 import sharded as S
+
+    local = device_of(args, local)
+    ctx = pk.Context(local, args.mode)
+    mq = pk.make_arch_quadrotor()
+    lo = np.array([-0.4] * 6 + [0.0] * 6)
+    prob = pk.ReachProblem(mq, pk.IntervalVector(lo, -lo), None, 0.0, 1.0, 0.01, 0)
+    m = 10 ** 6
+    b, e = S.mc_sample_range(m, world, rank)
+
+    def once():
+        flo = np.full((1, 12), np.inf)
+        fhi = np.full((1, 12), -np.inf)
+        pk.monte_carlo_range(prob, 1, b, e, flo, fhi, ctx=ctx)
+        if world > 1:
+            tl, th = torch.from_numpy(flo), torch.from_numpy(fhi)
+            if dist.get_backend() != "gloo":
+                tl, th = tl.cuda(local), th.cuda(local)
+            S.allreduce_hull(tl, th)
+            flo, fhi = tl.cpu().numpy(), th.cpu().numpy()
+        return flo, fhi
+
+    once()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    flo, fhi = once()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64, device=torch.device("cuda", local))
+    if world > 1:
+        allreduce(dist, t, dist.ReduceOp.MAX)
+    ctx.close()
+    ok = bool(np.isfinite(flo).all() and np.isfinite(fhi).all() and (flo <= fhi).all())
+    return {"value": m * 100 / float(t.item()), "unit": "sample-steps/s", "seconds": float(t.item()),
+            "n_gpus": world, "samples": m, "hull_ok": ok, "scaling": "strong",
+            "workload": "C2 arch-quadrotor MC m=1e6, 100 steps, sample ranges per rank + MIN/MAX all-reduce"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -682,10 +726,12 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_baseline(args)
     if rank == 0 and world == 1 and not args.no_secondary:
         line["secondary"] = secondary(args, pk, torch)
-    if not args.no_secondary:  # config 4 at N GPUs (the N = 1 value is its baseline)
+    if not args.no_secondary:  # configs 4 and 2 at N GPUs (the N = 1 values are their baselines)
         c4n = sharded_chain_bench(args, world, rank, local, torch, pk, dist)
+        c2n = sharded_mc_bench(args, world, rank, local, torch, pk, dist)
         if rank == 0:
             line.setdefault("secondary", {})["C4_chain_sharded_nGPU"] = c4n
+            line["secondary"]["C2_mc_sharded_nGPU"] = c2n
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

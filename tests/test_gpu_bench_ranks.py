@@ -2,7 +2,8 @@
 two ranks on cuda:0 (--same-device, gloo with host-staged halos) at a reduced
 grid.  Exercises the sharded device bench (z-slab halos, interior/boundary
 split), the sharded e2e call, the sharded C4 chain line and every max-over-ranks
-reduction -- the code the driver's 8-GPU scaling run executes with NCCL."""
+reduction, the sharded Monte Carlo line -- the code the driver's 8-GPU scaling
+run executes with NCCL."""
 import json
 import os
 import subprocess
@@ -31,3 +32,5 @@ def test_bench_two_ranks_one_gpu():
     assert e2e["value"] > 0 and not e2e["order_violated"] and e2e["rk4_steps"] == 100
     c4 = line["secondary"]["C4_chain_sharded_nGPU"]
     assert c4["n_gpus"] == 2 and c4["value"] > 0
+    c2 = line["secondary"]["C2_mc_sharded_nGPU"]
+    assert c2["n_gpus"] == 2 and c2["hull_ok"] and c2["value"] > 0
