@@ -114,6 +114,12 @@ pirk_status pirk_program_create(const char* source, uint64_t dim, uint64_t input
  * log.  *cubin_bytes (may be NULL) receives the size of the sm_100a image. */
 pirk_status pirk_program_compile(pirk_program* prog, int32_t mode, char* log, size_t log_len,
                                  uint64_t* cubin_bytes);
+/* Declare the model a radius-r 1-D stencil: f_i, d_i and g_i read only
+ * components in [i - r, i + r] of each state argument (plus the inputs).  MM
+ * and GB then advance one whole RK4 step per launch with a shared-memory tile
+ * of both fields and a 4r halo (16 B of HBM per state-update) instead of four
+ * stage launches.  1 <= r <= 64; call before the first compile. */
+pirk_status pirk_program_set_stencil(pirk_program* prog, uint64_t radius);
 /* Copy the compiled sm_100a cubin of `mode` (after pirk_program_compile). */
 pirk_status pirk_program_cubin(const pirk_program* prog, int32_t mode, void* buf, uint64_t len);
 void pirk_program_destroy(pirk_program* prog);

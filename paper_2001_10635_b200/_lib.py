@@ -139,6 +139,7 @@ SIGNATURES = {
                                       C.POINTER(C.c_void_p)]),
     "pirk_program_compile": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_size_t, _U64P]),
     "pirk_program_cubin": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_uint64]),
+    "pirk_program_set_stencil": (C.c_int, [C.c_void_p, C.c_uint64]),
     "pirk_program_destroy": (None, [C.c_void_p]),
     "pirk_step_window": (C.c_int, [C.c_void_p, _MP, C.c_int32, C.POINTER(PirkWindow), _DP, _DP,
                                    C.c_double, C.c_double, C.c_uint64, C.c_void_p]),

@@ -40,13 +40,15 @@ struct UserBuild {
     std::string log;
     std::vector<char> cubin;
     cudaLibrary_t lib = nullptr;
-    cudaKernel_t k_small = nullptr, k_stage = nullptr, k_mc = nullptr;
+    cudaKernel_t k_small = nullptr, k_stage = nullptr, k_mc = nullptr, k_tile = nullptr;
+    unsigned long long tile_devices = 0;  // devices the tile kernel's smem opt-in is set on
 };
 
 struct pirk_program {
     std::string source;
     uint64_t dim = 0, input_dim = 0;
     uint32_t flags = 0;
+    uint64_t stencil = 0;  // pirk_program_set_stencil: radius of a 1-D stencil model (0 = unknown)
     std::mutex mu;
     UserBuild build[2];  // [pirk_mode]
     ~pirk_program() {
@@ -2062,6 +2064,14 @@ pirk_status pirk_program_cubin(const pirk_program* pg, int32_t mode, void* buf, 
     const UserBuild& b = pg->build[mode == PIRK_MODE_EXACT ? 0 : 1];
     if (!b.ok || len < b.cubin.size()) return PIRK_EINVAL;
     std::memcpy(buf, b.cubin.data(), b.cubin.size());
+    return PIRK_OK;
+}
+
+pirk_status pirk_program_set_stencil(pirk_program* pg, uint64_t radius) {
+    if (!pg || radius > kUserStencilMax) return PIRK_EINVAL;
+    std::lock_guard<std::mutex> lk(pg->mu);
+    if (pg->build[0].tried || pg->build[1].tried) return PIRK_EINVAL;  // before the first compile
+    pg->stencil = radius;
     return PIRK_OK;
 }
 

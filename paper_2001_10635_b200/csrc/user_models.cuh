@@ -35,7 +35,8 @@ bool user_compile(pirk_program* pg, int mode, UserBuild& b) {
         "-DPIRK_N=" + std::to_string(pg->dim) + "ull", "-DPIRK_NI=" + std::to_string(pg->input_dim) + "ull",
         "-DPIRK_HAS_RHS=" + std::to_string((pg->flags & PIRK_HAS_RHS) ? 1 : 0),
         "-DPIRK_HAS_DECOMP=" + std::to_string((pg->flags & PIRK_HAS_DECOMPOSITION) ? 1 : 0),
-        "-DPIRK_HAS_GROWTH=" + std::to_string((pg->flags & PIRK_HAS_GROWTH) ? 1 : 0)};
+        "-DPIRK_HAS_GROWTH=" + std::to_string((pg->flags & PIRK_HAS_GROWTH) ? 1 : 0),
+        "-DPIRK_STENCIL=" + std::to_string(pg->stencil)};
     std::vector<const char*> ov;
     for (const std::string& o : opt) ov.push_back(o.c_str());
     const nvrtcResult cr = nvrtcCompileProgram(prog, static_cast<int>(ov.size()), ov.data());
@@ -72,6 +73,7 @@ pirk_status user_kernels(pirk_ctx* ctx, const pirk_model* m, UserBuild** out) {
         CK(ctx, cudaLibraryGetKernel(&b.k_small, b.lib, "pirk_user_small"));
         CK(ctx, cudaLibraryGetKernel(&b.k_stage, b.lib, "pirk_user_stage"));
         CK(ctx, cudaLibraryGetKernel(&b.k_mc, b.lib, "pirk_user_mc"));
+        if (pg->stencil > 0) CK(ctx, cudaLibraryGetKernel(&b.k_tile, b.lib, "pirk_user_tile"));
     }
     *out = &b;
     return PIRK_OK;
@@ -103,6 +105,28 @@ cudaError_t user_launch_stage(UserBuild* b, int which, int stage, double t0, dou
                             dim3(256), args, 0, stream);
 }
 
+size_t user_tile_smem(uint64_t radius) { return 8 * (kUserTile + 8 * radius) * sizeof(double); }
+
+cudaError_t user_launch_tile(UserBuild* b, uint64_t radius, int which, double t0, double t1, double h,
+                             unsigned long long step, unsigned long long total, const double* in0,
+                             const double* in1, double* out0, double* out1, const double* p, unsigned long long n,
+                             unsigned long long* fail, cudaStream_t stream) {
+    const size_t smem = user_tile_smem(radius);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (!(b->tile_devices & (1ull << (dev & 63)))) {  // dynamic shared memory opt-in, per device
+        e = cudaKernelSetAttributeForDevice(b->k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            static_cast<int>(smem), dev);
+        if (e != cudaSuccess) return e;
+        b->tile_devices |= 1ull << (dev & 63);
+    }
+    void* args[] = {&which, &t0, &t1, &h, &step, &total, &in0, &in1, &out0, &out1, &p, &n, &fail};
+    return cudaLaunchKernel(reinterpret_cast<const void*>(b->k_tile),
+                            dim3(static_cast<unsigned>((n + kUserTile - 1) / kUserTile)), dim3(kUserTileThreads),
+                            args, smem, stream);
+}
+
 // MM / GB of a user model with n > kUserSmallMax: one thread per component,
 // four stage launches per RK4 step (pirk_user_stage), any stencil the
 // evaluators read.  Slots go straight to the caller's tube; GB composes the
@@ -126,6 +150,9 @@ pirk_status run_user_large(pirk_ctx* ctx, const pirk_model* m, int method, const
     const uint64_t n = m->dim, ni = m->input_dim;
     const bool mm = method == PIRK_METHOD_MM;
     const uint64_t D = mm ? 2 * n : n;
+    // radius-r stencil models: one fused step per launch on ping-pong field
+    // buffers (X holds [field 0 | field 1], UA the other copy)
+    const bool tiled = user_program(m)->stencil > 0 && ub->k_tile;
     DevBuf<double> X, UA, UB, ACC, P;
     DevBuf<unsigned long long> dfail, sflag;
     CK(ctx, X.alloc(ctx, D));
@@ -169,6 +196,15 @@ pirk_status run_user_large(pirk_ctx* ctx, const pirk_model* m, int method, const
         uint64_t done = 0;
         for (uint64_t s = 0; s < S; ++s) {
             for (; done < slot_steps[s]; ++done) {
+                if (tiled) {  // X -> UA in one launch, then swap (the copy back keeps X the state)
+                    const uint64_t nn = n;
+                    CK(ctx, user_launch_tile(ub, user_program(m)->stencil, which, p->t0, p->t1, p->h, done,
+                                             plan.total, X.p, X.p + nn, UA.p, UA.p + nn, P.p, nn,
+                                             dfail.p + pass, ctx->stream));
+                    ctx->launches++;
+                    std::swap(X.p, UA.p);
+                    continue;
+                }
                 const double* ins[4] = {X.p, UA.p, UB.p, UA.p};
                 double* outs[4] = {UA.p, UB.p, UA.p, nullptr};
                 for (int stg = 0; stg < 4; ++stg) {

@@ -22,6 +22,11 @@
 //                       component (any n): 4 launches per step
 //   pirk_user_mc     -- Monte Carlo, one sample per thread (reach.cpp:246-323),
 //                       hull folded with warp shuffles + ordered-key atomics
+//   pirk_user_tile   -- a whole RK4 step per launch for models declared as
+//                       radius-r 1-D stencils (pirk_program_set_stencil): a CTA
+//                       stages its tile of both fields plus a 4r halo in shared
+//                       memory and runs the four stages there (16 B of HBM per
+//                       state-update instead of the stage kernels' ~100)
 #pragma once
 
 namespace pirk {
@@ -31,6 +36,11 @@ constexpr unsigned long long kUserSmallMax = 64;
 // Monte Carlo keeps a sample's state in registers/local memory; the failure
 // key packs the component into 10 bits
 constexpr unsigned long long kUserMcMax = 1024;
+// radius-r tile kernel: outputs per CTA and threads; shared memory holds
+// 2 fields x 4 arrays (x, u ping-pong, acc) x (kUserTile + 8 r) doubles
+constexpr unsigned long long kUserTile = 1024;
+constexpr unsigned kUserTileThreads = 256;
+constexpr unsigned long long kUserStencilMax = 64;
 
 static const char* kUserPrelude = R"PIRK(
 typedef unsigned long long u64;
@@ -186,6 +196,88 @@ extern "C" __global__ void pirk_user_stage(int which, int stage, double t0, doub
         if (!pirk_rt::finite_d(xn)) atomicMin(fail, (step << pirk_rt::kFailCompBits) | i);
     }
 }
+
+// One RK4 step of a radius-R 1-D stencil model (pirk_program_set_stencil): the
+// CTA owns outputs [c0, c1) and stages x on [lo, hi) = [c0 - 4R, c1 + 4R) of
+// both fields (clamped to the domain).  Stage s is evaluated on the range that
+// shrinks by R per stage away from the domain ends (the 4-stage dependency
+// cone), in shared memory, with the expressions and stage times of
+// pirk_user_stage (rk4.cpp:50-75): bit-identical to it.  The user functions
+// see pointers rebased so that x[i] is component i.
+//   which 0: f on field 0 (p); 1: g on field 0 (w); 2: the embedding, field 0
+//   = x under d(x, p, xh, ph), field 1 = xh under d(xh, ph, x, p)
+#if PIRK_STENCIL > 0
+extern "C" __global__ void __launch_bounds__(256) pirk_user_tile(int which, double t0, double t1, double h,
+        u64 step, u64 total, const double* __restrict__ in0, const double* __restrict__ in1,
+        double* __restrict__ out0, double* __restrict__ out1, const double* __restrict__ p, u64 n,
+        u64* fail) {
+    constexpr long long R = PIRK_STENCIL;
+    constexpr long long TO = 1024;
+    constexpr long long L = TO + 8 * R;
+    extern __shared__ double sm[];
+    const int nf = which == 2 ? 2 : 1;
+    const long long c0 = (long long)blockIdx.x * TO;
+    long long c1 = c0 + TO;
+    if (c1 > (long long)n) c1 = (long long)n;
+    const long long lo = c0 - 4 * R > 0 ? c0 - 4 * R : 0;
+    const long long hi = c1 + 4 * R < (long long)n ? c1 + 4 * R : (long long)n;
+    double* X[2];
+    double* UA[2];
+    double* UB[2];
+    double* AC[2];
+    for (int f = 0; f < 2; ++f) {
+        X[f] = sm + (4 * f + 0) * L;
+        UA[f] = sm + (4 * f + 1) * L;
+        UB[f] = sm + (4 * f + 2) * L;
+        AC[f] = sm + (4 * f + 3) * L;
+    }
+    for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        X[0][i - lo] = in0[i];
+        if (nf == 2) X[1][i - lo] = in1[i];
+    }
+    __syncthreads();
+    const pirk_rt::StepConsts c = pirk_rt::step_consts(t0, t1, h, step, total);
+    const double* P0 = p;
+    const double* P1 = p + PIRK_NI;
+    for (int stage = 0; stage < 4; ++stage) {
+        // valid range of this stage's output: shrinks by R per stage, not at the domain ends
+        const long long a = lo == 0 ? 0 : lo + (stage + 1) * R;
+        const long long b = hi == (long long)n ? (long long)n : hi - (stage + 1) * R;
+        const double tt = stage == 0 ? c.t : (stage == 3 ? c.thk : c.th2);
+        for (long long i = a + threadIdx.x; i < b; i += blockDim.x) {
+            const long long o = i - lo;
+            for (int f = 0; f < nf; ++f) {
+                const double* S0 = (stage == 0 ? X[0] : UA[0]) - lo;   // rebased: S0[j] is component j
+                const double* S1 = (stage == 0 ? X[1] : UA[1]) - lo;
+                double k;
+                if (which == 0) k = pirk_rhs((u64)i, tt, S0, P0);
+                else if (which == 1) k = pirk_growth((u64)i, tt, S0, P0);
+                else if (f == 0) k = pirk_decomposition((u64)i, tt, S0, P0, S1, P1);
+                else k = pirk_decomposition((u64)i, tt, S1, P1, S0, P0);
+                const double x = X[f][o];
+                if (stage == 0) {
+                    AC[f][o] = k;
+                    UB[f][o] = x + c.h2 * k;
+                } else if (stage < 3) {
+                    AC[f][o] = AC[f][o] + 2.0 * k;
+                    UB[f][o] = x + (stage == 1 ? c.h2 : c.hk) * k;
+                } else if (i >= c0 && i < c1) {
+                    const double xn = x + c.h6 * (AC[f][o] + k);
+                    (f == 0 ? out0 : out1)[i] = xn;
+                    if (!pirk_rt::finite_d(xn))
+                        atomicMin(fail, (step << pirk_rt::kFailCompBits) | ((u64)i + (which == 2 && f == 1 ? n : 0ull)));
+                }
+            }
+        }
+        __syncthreads();
+        for (int f = 0; f < 2; ++f) {
+            double* tmp = UA[f];
+            UA[f] = UB[f];
+            UB[f] = tmp;
+        }
+    }
+}
+#endif
 
 struct UserMcArgs {
     const double* lo;

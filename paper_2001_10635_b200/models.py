@@ -59,7 +59,7 @@ class Program:
     use (exact mode: --fmad=false).  ``compile(mode)`` compiles eagerly and
     raises ValueError with the NVRTC log on a bad source (no GPU needed)."""
 
-    def __init__(self, source: str, dim: int, input_dim: int, flags: int):
+    def __init__(self, source: str, dim: int, input_dim: int, flags: int, stencil_radius: int = 0):
         import ctypes as C
 
         from . import _lib
@@ -70,6 +70,10 @@ class Program:
         if st != _lib.OK:
             raise ValueError("pirk_program_create: invalid source or dimension")
         self._h = h
+        if stencil_radius:
+            if _lib.lib().pirk_program_set_stencil(h, int(stencil_radius)) != _lib.OK:
+                raise ValueError("user model: stencil radius must lie in [1, 64]")
+        self.stencil_radius = int(stencil_radius)
         self.source = source
         self.dim = int(dim)
         self.input_dim = int(input_dim)
@@ -117,15 +121,17 @@ class Program:
 def make_user_model(source: str, dim: int, input_dim: int = 0, *, rhs: bool = True,
                     decomposition: bool = False, growth: bool = False,
                     input_affine: bool = False, name: str = "user",
-                    sparsity_note: str = "") -> SystemModel:
+                    sparsity_note: str = "", stencil_radius: int = 0) -> SystemModel:
     """A SystemModel with caller-written evaluators (system_model.hpp:28-43:
     ``rhs`` always, ``decomposition`` / ``growth_rhs`` optional, the
     ``input_affine`` flag growth-bound requires).  ``source`` is CUDA C++; see
-    :class:`Program`."""
+    :class:`Program`.  ``stencil_radius`` r > 0 declares a 1-D stencil (the
+    evaluators read components i-r .. i+r only): MM / GB then run one fused
+    RK4 step per launch (pirk_program_set_stencil)."""
     _require(dim >= 1, "user model needs at least 1 state")
     flags = ((HAS_RHS if rhs else 0) | (HAS_DECOMPOSITION if decomposition else 0)
              | (HAS_GROWTH if growth else 0) | (INPUT_AFFINE if input_affine else 0))
-    prog = Program(source, dim, input_dim, flags)
+    prog = Program(source, dim, input_dim, flags, stencil_radius)
     return SystemModel(USER, int(dim), int(input_dim), (), DECOMP_NATIVE if decomposition else DECOMP_NONE,
                        name=name, input_affine=input_affine, sparsity_note=sparsity_note, program=prog)
 

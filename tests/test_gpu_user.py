@@ -305,3 +305,47 @@ def test_user_nonfinite_reports_step(ctx):
     with pytest.raises(O.OracleError) as eo:
         O.mixed_monotonicity(cat, [1.0], [1.0], None, None, 0.0, 600.0, 10.0, 0)
     assert str(ei.value) == str(eo.value)
+
+
+CHAIN_SRC = r"""
+// SURVEY.md 8(d) C4 coupled chain (a = 1, b = 0.5, c = 0.25) as a user model
+__device__ double chain_s(double z) { return z / (1.0 + fabs(z)); }
+__device__ double pirk_decomposition(u64 i, double, const double* x, const double* p, const double* xh,
+                                     const double*) {
+    const double sl = (i == 0) ? 0.0 : chain_s(x[i - 1]);
+    const double sr = (i + 1 == PIRK_N) ? 0.0 : chain_s(xh[i + 1]);
+    return ((-1.0) * x[i] + 0.5 * sl - 0.25 * sr) + p[0];
+}
+__device__ double pirk_rhs(u64 i, double t, const double* x, const double* p) {
+    return pirk_decomposition(i, t, x, p, x, p);
+}
+"""
+
+
+@pytest.mark.parametrize("n", [65, 1024, 1025, 100003])
+def test_user_stencil_tile_path(mctx, n):
+    """Models declared as radius-1 stencils run one fused RK4 step per launch
+    (pirk_user_tile): traffic MM/GB and the coupled chain (whose decomposition
+    reads the other field) bit-identical to the oracle's catalog models."""
+    um = pk.make_user_model(TRAFFIC_SRC, n, 1, decomposition=True, growth=True, input_affine=True,
+                            stencil_radius=1)
+    up = traffic_prob(um, n)
+    cp = traffic_prob(pk.make_traffic(n), n)
+    for fn, ofn in ((pk.mixed_monotonicity, O.mixed_monotonicity), (pk.growth_bound, O.growth_bound)):
+        tube = fn(up, ctx=mctx)
+        assert tube.report.kernel_launches <= 12 + 12  # one launch per step (+ epilogues), not four
+        oref = ofn(pk.make_traffic(n), cp.initial.lower, cp.initial.upper, [4.0], [6.0], 0.0, 6.0, 0.5, 3)
+        if mctx.mode == "exact":
+            assert_bitexact(tube, oref)
+        else:
+            assert_within(tube, oref, rel=1e-12)
+    cm = pk.make_user_model(CHAIN_SRC, n, 1, decomposition=True, stencil_radius=1)
+    ctr = np.linspace(-1, 1, n)
+    prob = pk.ReachProblem(cm, pk.IntervalVector(ctr - 0.05, ctr + 0.05), pk.IntervalVector([-0.1], [0.1]),
+                           0.0, 0.3, 0.01, 10)
+    oref = O.mixed_monotonicity(pk.make_chain(n), ctr - 0.05, ctr + 0.05, [-0.1], [0.1], 0.0, 0.3, 0.01, 10)
+    tube = pk.mixed_monotonicity(prob, ctx=mctx)
+    if mctx.mode == "exact":
+        assert_bitexact(tube, oref)
+    else:
+        assert_within(tube, oref, rel=1e-12, atol=1e-15)

@@ -48,3 +48,19 @@ def test_flags_select_methods():
                            "{ return -x[0]; }", 1)
     assert not m.has_decomposition() and not m.has_growth()
     assert m.program.compile("fast") > 0
+
+
+def test_stencil_program_compiles_tile_kernel():
+    m = pk.make_user_model(SRC.replace("-x[i] + p[0]", "(i > 0 ? x[i - 1] : p[0]) - x[i]"), 100, 1,
+                           decomposition=True, growth=True, input_affine=True, stencil_radius=1)
+    img = m.program.cubin("exact")
+    with tempfile.NamedTemporaryFile(suffix=".cubin", delete=False) as f:
+        f.write(img)
+    try:
+        out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", f.name], capture_output=True,
+                             text=True).stdout
+    finally:
+        os.unlink(f.name)
+    assert "pirk_user_tile" in out
+    with pytest.raises(ValueError, match="stencil radius"):
+        pk.make_user_model(SRC, 10, 1, stencil_radius=65)
