@@ -15,6 +15,8 @@
 // sin/cos (arch-quadrotor), which CUDA does not reproduce bit-for-bit.
 #pragma once
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -309,13 +311,162 @@ __global__ void small_integrate_kernel(const SmallModel m, const int which, cons
     }
 }
 
+// ------------------------------------------- warp-parallel single-trajectory integrator
+//
+// The same integration as small_integrate_kernel with the components of each
+// stage spread over the 32 lanes of one warp (the reference parallelises
+// integrate_step over components the same way, rk4.cpp:47-76): lane l owns
+// components l, l+32, ...; the stage inputs live in shared memory (ping-pong,
+// so a stage reads one buffer while it writes the other), one __syncwarp per
+// stage.  Every component is evaluated with exactly the serial kernel's
+// expression, so results are bit-identical to it; the latency of a step drops
+// from D component evaluations in sequence to about one.
+
+// f_i alone (arch-quadrotor / Laub-Loomis evaluate all components together;
+// fast mode: the small-angle arch-quadrotor field of the MC kernel)
+template <bool Exact>
+static __device__ double sm_f_comp(const SmallModel& m, int i, const double* x, const double* p) {
+    if (m.kind == kArchQuad) {
+        double f[12];
+        if constexpr (Exact) aq_f_all(m, x, f);
+        else aq_f_all_fast(m, x, f);
+        return f[i];
+    }
+    if (m.kind == kLaubLoomis) {
+        double f[7];
+        ll_f_all(x, f);
+        return f[i];
+    }
+    return sm_f(m, i, x, p);
+}
+
+// embedding component c of [x | xh] (sm_embed_all, one component)
+template <bool Exact>
+static __device__ double sm_embed_comp(const SmallModel& m, int c, const double* y, const double* p) {
+    const int n = m.n, ni = m.ni;
+    const bool up = c >= n;
+    const int i = up ? c - n : c;
+    const double* xa = up ? y + n : y;
+    const double* xb = up ? y : y + n;
+    const double* pa = up ? p + ni : p;
+    if (m.kind == kChain) {
+        const double sl = (i == 0) ? 0.0 : xa[i - 1] / (1.0 + fabs(xa[i - 1]));
+        const double sr = (i + 1 == n) ? 0.0 : xb[i + 1] / (1.0 + fabs(xb[i + 1]));
+        return ((-m.P[0]) * xa[i] + m.P[1] * sl - m.P[2] * sr) + pa[0];
+    }
+    double a = sm_f_comp<Exact>(m, i, xa, pa);
+    if (m.decomp == kDecompJacobian) {
+        for (int j = 0; j < n; ++j) {
+            const double cij = m.C[i * n + j];
+            if (j == i || cij == 0.0) continue;
+            a = a + cij * (xa[j] - xb[j]);
+        }
+    }
+    return a;
+}
+
+template <bool Exact>
+static __device__ double sm_comp(const SmallModel& m, int which, int c, const double* y, const double* p) {
+    if (which == 0) return sm_f_comp<Exact>(m, c, y, p);
+    if (which == 1) return sm_g(m, c, y, p);
+    return sm_embed_comp<Exact>(m, c, y, p);
+}
+
+template <bool Exact>
+__global__ void __launch_bounds__(32) small_warp_kernel(const SmallModel m, const int which, const double* x0,
+                                                         const double* p, const double t0, const double t1,
+                                                         const double h, const unsigned long long total,
+                                                         const unsigned long long stride, double* rec,
+                                                         unsigned long long* fail) {
+    (void)sizeof(ModeCheck<Exact>);
+    constexpr int kMax = 2 * kSmallMax;
+    constexpr int kPer = kMax / 32;
+    __shared__ double X[kMax], UA[kMax], UB[kMax];
+    const int lane = threadIdx.x;
+    const int D = (which == 2) ? 2 * m.n : m.n;
+    double acc[kPer];
+    for (int q = 0; q < kPer; ++q) {
+        const int c = lane + 32 * q;
+        if (c < D) X[c] = x0[c];
+    }
+    __syncwarp();
+    unsigned long long slot = 0;
+    if (stride > 0) {
+        for (int q = 0; q < kPer; ++q) {
+            const int c = lane + 32 * q;
+            if (c < D) rec[c] = X[c];
+        }
+        slot = 1;
+    }
+    for (unsigned long long s = 0; s < total; ++s) {
+        const StepConsts sc = step_consts(t0, t1, h, s, total);
+        // stage 1: k0 = F(x); acc = k0; u1 = x + h2 k0
+        for (int q = 0; q < kPer; ++q) {
+            const int c = lane + 32 * q;
+            if (c >= D) continue;
+            const double k = sm_comp<Exact>(m, which, c, X, p);
+            acc[q] = k;
+            UA[c] = X[c] + sc.h2 * k;
+        }
+        __syncwarp();
+        // stage 2: k1 = F(u1); acc += 2 k1; u2 = x + h2 k1
+        for (int q = 0; q < kPer; ++q) {
+            const int c = lane + 32 * q;
+            if (c >= D) continue;
+            const double k = sm_comp<Exact>(m, which, c, UA, p);
+            acc[q] = acc[q] + 2.0 * k;
+            UB[c] = X[c] + sc.h2 * k;
+        }
+        __syncwarp();
+        // stage 3: k2 = F(u2); acc += 2 k2; u3 = x + hk k2
+        for (int q = 0; q < kPer; ++q) {
+            const int c = lane + 32 * q;
+            if (c >= D) continue;
+            const double k = sm_comp<Exact>(m, which, c, UB, p);
+            acc[q] = acc[q] + 2.0 * k;
+            UA[c] = X[c] + sc.hk * k;
+        }
+        __syncwarp();
+        // stage 4: k3 = F(u3); x = x + h6 (acc + k3) (no lane reads X in this stage)
+        unsigned bad = 0xffffffffu;
+        for (int q = 0; q < kPer; ++q) {
+            const int c = lane + 32 * q;
+            if (c >= D) continue;
+            const double k = sm_comp<Exact>(m, which, c, UA, p);
+            const double xn = X[c] + sc.h6 * (acc[q] + k);
+            X[c] = xn;
+            if (!finite_d(xn) && static_cast<unsigned>(c) < bad) bad = static_cast<unsigned>(c);
+        }
+        __syncwarp();
+        bad = __reduce_min_sync(0xffffffffu, bad);
+        if (bad != 0xffffffffu) {  // the reference throws at the first failing step, lowest component
+            if (lane == 0) record_fail(fail, s, static_cast<unsigned long long>(bad));
+            return;
+        }
+        if (s + 1 == total || (stride > 0 && (s + 1) % stride == 0)) {
+            for (int q = 0; q < kPer; ++q) {
+                const int c = lane + 32 * q;
+                if (c < D) rec[slot * D + c] = X[c];
+            }
+            ++slot;
+        }
+    }
+}
+
 template <bool Exact>
 cudaError_t launch_small_integrate(const SmallModel& m, int which, const double* x0,
                                    const double* p, double t0, double t1, double h,
                                    unsigned long long total, unsigned long long stride,
                                    double* rec, unsigned long long* fail, cudaStream_t stream) {
-    small_integrate_kernel<Exact><<<1, 32, 0, stream>>>(m, which, x0, p, t0, t1, h, total,
-                                                         stride, rec, fail);
+    // PIRK_SMALL_SERIAL=1: the one-thread kernel (A/B; both are bit-identical)
+    static const bool serial = [] {
+        const char* v = std::getenv("PIRK_SMALL_SERIAL");
+        return v && v[0] == '1';
+    }();
+    if (serial)
+        small_integrate_kernel<Exact><<<1, 32, 0, stream>>>(m, which, x0, p, t0, t1, h, total, stride, rec, fail);
+    else
+        small_warp_kernel<Exact><<<1, 32, 0, stream>>>(m, which, x0, p, t0, t1, h, total, stride, rec, fail);
     return cudaGetLastError();
 }
 

@@ -577,3 +577,27 @@ def test_heat_pipelined_final_box(mode):
             pk.mixed_monotonicity(prob2, ctx=c)
     finally:
         c.close()
+
+
+def test_small_serial_kernel_variant():
+    """The one-thread small-system integrator (PIRK_SMALL_SERIAL=1) and the
+    default warp-parallel one give the same results: the small-system tests
+    rerun in a child process with the serial kernel."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PIRK_SMALL_SERIAL="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        os.path.join(root, "tests", "test_gpu_parity.py"),
+                        "-k", "scalar or laub or arch_quad_gb or arch_quad_ctmm or frozen or golden"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_arch_quad_fast_mode_small_integrator(fast_ctx):
+    """Fast mode: the warp-parallel small integrator evaluates the arch-quadrotor
+    with the small-angle sincos of the MC kernel -- GB and CTMM within the
+    tolerance contract of the glibc-trig oracle."""
+    m, prob = arch_quad_problem()
+    assert_within(pk.growth_bound(prob, ctx=fast_ctx), oracle_for("gb", prob), rel=1e-12, atol=1e-14)
+    m, prob = arch_quad_problem(decomp=True)
+    assert_within(pk.mixed_monotonicity(prob, ctx=fast_ctx), oracle_for("mm", prob), rel=1e-12, atol=1e-14)
