@@ -676,13 +676,15 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
         r.tt = tt;                                                                                   \
         r.run();                                                                                     \
     }
-#ifdef PIRK_STRIP_TIMING_ONLY_INTERIOR  // A/B timing only: every tile runs the interior code (wrong at edges)
-    if (true) PIRK_STRIP_RUN(0)
+#if defined(PIRK_STRIP_TIMING_ONLY_INTERIOR)  // A/B timing only: every tile runs the interior code (wrong at edges)
+    PIRK_STRIP_RUN(0)
+#elif defined(PIRK_STRIP_TIMING_SKIP_EDGES)  // A/B timing only: edge tiles do nothing
+    if (interior) PIRK_STRIP_RUN(0)
 #else
     if (interior) PIRK_STRIP_RUN(0)
-#endif
     else if (PIRK_STRIP_EDGECSE && g % 4 == 0) PIRK_STRIP_RUN(1)
     else PIRK_STRIP_RUN(2)
+#endif
 #undef PIRK_STRIP_RUN
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
     tmem_fence_before();
