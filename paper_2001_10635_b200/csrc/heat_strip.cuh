@@ -680,6 +680,9 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
     PIRK_STRIP_RUN(0)
 #elif defined(PIRK_STRIP_TIMING_SKIP_EDGES)  // A/B timing only: edge tiles do nothing
     if (interior) PIRK_STRIP_RUN(0)
+#elif defined(PIRK_STRIP_TIMING_NO_KIND2)  // A/B timing only: no generic edge path (g % 4 == 0 only)
+    if (interior) PIRK_STRIP_RUN(0)
+    else PIRK_STRIP_RUN(1)
 #else
     if (interior) PIRK_STRIP_RUN(0)
     else if (PIRK_STRIP_EDGECSE && g % 4 == 0) PIRK_STRIP_RUN(1)
