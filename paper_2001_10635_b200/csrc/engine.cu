@@ -1011,14 +1011,16 @@ pirk_status run_large(pirk_ctx* ctx, const pirk_model* m, int method, const pirk
 // copy stream).  Chains shard contiguous component ranges, heat3d contiguous
 // z-slabs (models.cpp:110-112), exactly as sharded.py does across processes.
 // Each lane keeps a window of its units plus a 4-unit halo per side (the RK4
-// dependency cone of a radius-1 stencil) and exchanges halos every step by
-// copy-engine peer copies over NVLink:
+// dependency cone of a radius-1 stencil) and exchanges halos every step.  By
+// default the boundary launch itself stores its units into the neighbours'
+// halos over NVLink peer memory (WindowArgs::mir0/1); PIRK_LANE_HALO=copy, or
+// lanes without peer access, use copy-engine peer copies instead:
 //
-//   lane stream:  wait(halos of step k-1) | boundary units | interior units ....
-//   lane copies:                          | send boundary -> neighbours' halos
+//   lane stream:  wait(halos of step k-1) | boundary units (+ peer stores) | interior ....
+//   lane copies:                          | (copy mode) send boundary -> neighbours' halos
 //
 // The boundary units (the ones the neighbours need next step) are computed
-// first, their peer copies run while the interior computes, and the next
+// first, their transfer overlaps the interior, and the next
 // step waits only for the copies (double-buffered events: a lane waits on
 // its neighbours' step-(k-1) records, never on the current ones).  Every unit
 // is computed once from the same inputs as on one device, so the result is
