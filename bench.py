@@ -2,8 +2,9 @@
 
 Default workload (BASELINE.json config 5 / north-star target): CTMM
 (mixed monotonicity) of heat3d with grid = 1600 (n = 4.096e9, embedding state
-2n = 8.19e9 fp64), h = 5e-8, strong-scaled over N GPUs as z-slabs with NCCL
-halo exchange.  One bench "step" is one RK4 step of the whole embedding.
+2n = 8.19e9 fp64), h = 5e-8, strong-scaled over N GPUs as z-slabs whose
+boundary launches store their halo planes straight into the neighbours'
+windows over NVLink (--halo peer; --halo nccl: NCCL send/recv).  One bench "step" is one RK4 step of the whole embedding.
 
 * value  -- state-updates/s (2n per step) with the state resident in HBM,
             CUDA events on the launching stream, max over ranks.
@@ -134,6 +135,21 @@ def device_of(args, local):
     return 0 if args.same_device else local
 
 
+def halo_exchanger(args, S, shard, unit, ctx, world):
+    """N > 1 halo transport of the heat runs: peer stores fused into the
+    boundary launches (--halo peer, default: CUDA IPC over NVLink, no
+    separate transfer) or NCCL send/recv (--halo nccl)."""
+    if world == 1:
+        return None
+    if args.halo == "peer":
+        return S.PeerStores(shard, unit, ctx)
+    return S.HaloExchanger(shard, unit)
+
+
+HALO_DESC = {"peer": "halos stored into the neighbours' windows by the boundary launches (CUDA IPC peer memory)",
+             "nccl": "NCCL halo exchange"}
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -153,12 +169,14 @@ def heat_device_bench(args, world, rank, local, torch, pk, dist):
     K = 1
     shard = S.Shard(args.grid, world, rank, 4 * K)
     unit = args.grid * args.grid
-    ex = S.HaloExchanger(shard, unit) if world > 1 else None
+    ex = halo_exchanger(args, S, shard, unit, ctx, world)
     step_fn = S.device_step_fn(model, "mixed-monotonicity", ctx)
     run = S.ShardedReach(model, "mixed-monotonicity", shard, step_fn, ex, K=K)
     dev = torch.device("cuda", local)
     fail = torch.full((2,), -1, dtype=torch.int64, device=dev)  # device failure keys
     a = run.alloc(lambda n: torch.empty(n, dtype=torch.float64, device=dev), fail=fail)
+    if isinstance(ex, S.PeerStores):
+        ex.attach(run)
     a[0].fill_(0.9)  # catalog default box [0.9, 1.1] (models.cpp:744-745)
     a[1].fill_(1.1)
     steps = [(float(k) * args.h, args.h) for k in range(args.warmup + args.steps)]
@@ -192,6 +210,8 @@ def heat_device_bench(args, world, rank, local, torch, pk, dist):
     ms_max = float(t.item())
     run.check(0.0, args.h)  # raises the reference's IntegrationError on any rank's failure
     check = state_check(run, args, torch, dist, world)
+    if isinstance(ex, S.PeerStores):
+        ex.close()
     del a, run
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
@@ -298,8 +318,8 @@ def heat_e2e(args, pk, torch, world):
 def heat_e2e_sharded(args, pk, torch, dist, world, rank, local):
     """N > 1 end to end: the full C5 reach (100 steps) through the sharded
     public API with host buffers per rank.  Each rank uploads its window of the
-    initial box from page-locked host memory, integrates with NCCL halo
-    exchange, checks the embedding order on its slab and downloads its slab of
+    initial box from page-locked host memory, integrates with the --halo
+    transport (peer stores or NCCL), checks the embedding order on its slab and downloads its slab of
     the final box; time = max over ranks of the whole call."""
     from paper_2001_10635_b200 import sharded as S
 
@@ -320,11 +340,14 @@ def heat_e2e_sharded(args, pk, torch, dist, world, rank, local):
     host[0].fill(0.9)
     host[1].fill(1.1)
     h_lo, h_hi, o_lo, o_hi = (torch.from_numpy(b) for b in host)
+    ex = halo_exchanger(args, S, shard, unit, ctx, world)
     run = S.ShardedReach(model, "mixed-monotonicity", shard, S.device_step_fn(model, "mixed-monotonicity", ctx),
-                         S.HaloExchanger(shard, unit), K=1)
+                         ex, K=1)
     steps = S.plan_rk4_steps(0.0, C5_STEPS * args.h, args.h)
     fail = torch.full((2,), -1, dtype=torch.int64, device=dev)
     a = run.alloc(lambda k: torch.empty(k, dtype=torch.float64, device=dev), fail=fail)
+    if isinstance(ex, S.PeerStores):
+        ex.attach(run)
     stream = torch.cuda.Stream(device=dev)
 
     def once():
@@ -353,8 +376,10 @@ def heat_e2e_sharded(args, pk, torch, dist, world, rank, local):
     res = {"value": 2.0 * n * len(steps) / tt[0].item(), "unit": UNIT,
            "h2d_bytes_per_step": 2 * 8 * (n + 2 * (world - 1) * 4 * unit), "d2h_bytes_per_step": 2 * n * 8,
            "seconds": tt[0].item(), "rk4_steps": len(steps), "n": n, "grid": g,
-           "api": "paper_2001_10635_b200.sharded.ShardedReach (one process per GPU, NCCL halos)",
+           "api": f"paper_2001_10635_b200.sharded.ShardedReach (one process per GPU, {HALO_DESC[args.halo]})",
            "order_violated": bool(tt[1].item()), "timing": "wall clock of the whole call, max over ranks"}
+    if isinstance(ex, S.PeerStores):
+        ex.close()
     del a, run, h_lo, h_hi, o_lo, o_hi
     for b in host:
         cudart.cudaHostUnregister(b.ctypes.data)
@@ -689,7 +714,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"CTMM heat3d grid={args.grid} (n={n}), embedding 2n, "
-                               f"h={args.h}, z-slab sharded with NCCL halo exchange",
+                               f"h={args.h}" + (f", z-slab sharded, {HALO_DESC[args.halo]}" if world > 1 else ""),
                    "mode": args.mode, "grid": args.grid, "n": n, "state_bytes": 32 * n,
                    "l2": "inputs (65.5 GB) far larger than the 126 MB L2; no flush needed",
                    "parallelism": f"zslab{world}"},
@@ -816,6 +841,9 @@ def main():
     ap.add_argument("--same-device", action="store_true",
                     help="every rank on cuda:0 (tests the N > 1 code path on one GPU; with --backend gloo)")
     ap.add_argument("--chain-n", type=int, default=10 ** 7)
+    ap.add_argument("--halo", default="peer", choices=["peer", "nccl"],
+                    help="N > 1 heat halo transport: peer stores fused into the boundary launches "
+                         "(CUDA IPC) or NCCL send/recv")
     ap.add_argument("--launcher-check", action="store_true",
                     help="print each rank's (rank, world) and exit: tests the --gpus relaunch without GPUs")
     args = ap.parse_args()

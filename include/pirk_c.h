@@ -188,8 +188,9 @@ pirk_status pirk_create(int device, pirk_ctx** out);
 /* A context of n_lanes shard lanes, lane r on CUDA device devices[r] (ids may
  * repeat: several lanes then share one GPU).  Chain and heat3d MM/GB runs
  * shard the state across the lanes (contiguous component ranges / z-slabs,
- * 4-unit halos exchanged every RK4 step by peer copies over NVLink, boundary
- * units first so the copies overlap the interior); Monte Carlo shards the
+ * 4-unit halos exchanged every RK4 step: the boundary launches store their
+ * units into the neighbours' halos over NVLink peer memory, then the interior
+ * runs; peer copies where peer access is missing); Monte Carlo shards the
  * sample range and min/max-folds the hulls.  Results are bit-identical for
  * any lane count.  This is what the reference's `workers` argument maps to
  * (reach.hpp:48,53,70).  Lane 0 is the primary device (pirk_set_stream). */
@@ -286,6 +287,34 @@ typedef struct pirk_window {
 pirk_status pirk_step_window(pirk_ctx* ctx, const pirk_model* model, int32_t method,
                              const pirk_window* win, const double* p0, const double* p1,
                              double t, double hk, uint64_t step_index, uint64_t* fail);
+
+/* ---- one process per GPU: halos by peer stores (replaces the shared address
+ * space the reference's OpenMP workers integrate in, rk4.cpp:47-75) ----
+ * A rank's boundary launch also stores its output units into the neighbour's
+ * window over NVLink and then raises the neighbour's step flag; the
+ * neighbour's stream waits for the flag before its next boundary launch.
+ *
+ * pirk_step_window_mirror: pirk_step_window that stores every output unit a
+ *   second time, to mir0 / mir1 (indexed like out0 / out1: mir0[0] is unit
+ *   out_begin; typically a peer process's window opened with pirk_ipc_open).
+ * pirk_ipc_export: IPC handle (64 bytes) of the allocation holding dptr and the
+ *   byte offset of dptr inside it (dptr may be a sub-allocation, e.g. torch's).
+ * pirk_ipc_open: map a peer process's allocation on `device`; returns its base
+ *   (add the exported offset).  Mapping the same handle again returns the same
+ *   base (reference-counted); pirk_ipc_close unmaps when the count drops to 0.
+ * pirk_wait_flag: the ctx stream waits until (int32_t)(*flag - value) >= 0;
+ *   flag is a uint32 in this process's device memory.
+ * pirk_signal_flag: after all prior work on the ctx stream, *flag = value
+ *   (system-scope release; flag may be a peer process's memory). */
+pirk_status pirk_step_window_mirror(pirk_ctx* ctx, const pirk_model* model, int32_t method,
+                                    const pirk_window* win, double* mir0, double* mir1,
+                                    const double* p0, const double* p1, double t, double hk,
+                                    uint64_t step_index, uint64_t* fail);
+pirk_status pirk_ipc_export(const void* dptr, unsigned char handle[64], uint64_t* offset);
+pirk_status pirk_ipc_open(int device, const unsigned char handle[64], void** base);
+pirk_status pirk_ipc_close(void* base);
+pirk_status pirk_wait_flag(pirk_ctx* ctx, const uint32_t* flag, uint32_t value);
+pirk_status pirk_signal_flag(pirk_ctx* ctx, uint32_t* flag, uint32_t value);
 
 #ifdef __cplusplus
 }

@@ -143,6 +143,14 @@ SIGNATURES = {
     "pirk_program_destroy": (None, [C.c_void_p]),
     "pirk_step_window": (C.c_int, [C.c_void_p, _MP, C.c_int32, C.POINTER(PirkWindow), _DP, _DP,
                                    C.c_double, C.c_double, C.c_uint64, C.c_void_p]),
+    "pirk_step_window_mirror": (C.c_int, [C.c_void_p, _MP, C.c_int32, C.POINTER(PirkWindow),
+                                          C.c_void_p, C.c_void_p, _DP, _DP, C.c_double, C.c_double,
+                                          C.c_uint64, C.c_void_p]),
+    "pirk_ipc_export": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_uint64)]),
+    "pirk_ipc_open": (C.c_int, [C.c_int, C.c_char_p, C.POINTER(C.c_void_p)]),
+    "pirk_ipc_close": (C.c_int, [C.c_void_p]),
+    "pirk_wait_flag": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32]),
+    "pirk_signal_flag": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32]),
 }
 
 # pirk_record_fn (include/pirk_c.h)

@@ -8,6 +8,7 @@
 // the state runs in the device kernels; the host only plans, launches,
 // transfers and formats.  There is no CPU fallback: an unsupported model or
 // a missing device is an error.
+#include <cuda.h>  // driver types for the entry points taken via cudaGetDriverEntryPoint
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
@@ -1996,9 +1997,10 @@ void pirk_engine_destroy(pirk_engine* e) {
     delete e;
 }
 
-pirk_status pirk_step_window(pirk_ctx* ctx, const pirk_model* m, int32_t method,
-                             const pirk_window* win, const double* p0, const double* p1,
-                             double t, double hk, uint64_t step_index, uint64_t* fail_ptr) {
+namespace {
+pirk_status step_window_impl(pirk_ctx* ctx, const pirk_model* m, int32_t method, const pirk_window* win,
+                             double* mir0, double* mir1, const double* p0, const double* p1, double t,
+                             double hk, uint64_t step_index, uint64_t* fail_ptr) {
     if (!ctx || !win) return PIRK_EINVAL;
     LOCK(ctx);
     pirk_status st = PIRK_OK;
@@ -2027,9 +2029,149 @@ pirk_status pirk_step_window(pirk_ctx* ctx, const pirk_model* m, int32_t method,
     sc.h6 = hk / 6.0;
     const ChainModel cm = chain_model(m, method, q0, q1);
     const HeatModel hm = heat_model(m, method);
+    if ((mir0 == nullptr) != (mir1 == nullptr))
+        return fail(ctx, PIRK_EINVAL, "step_window: mirror needs both fields");
     WindowArgs w{win->in0, win->in1, win->out0, win->out1, wb, we, win->out_begin, win->out_end};
+    w.mir0 = mir0;
+    w.mir1 = mir1;
     CK(ctx, step_launch(ctx, ctx->stream, m, cm, hm, w, sc, step_index,
                         reinterpret_cast<unsigned long long*>(fail_ptr)));
+    return PIRK_OK;
+}
+
+// driver entry points (no link-time libcuda dependency)
+struct DriverFns {
+    decltype(&cuStreamWaitValue32) wait32 = nullptr;
+    decltype(&cuMemGetAddressRange) range = nullptr;
+    bool ok = false;
+};
+const DriverFns& driver_fns() {
+    static DriverFns f = [] {
+        DriverFns d;
+        cudaDriverEntryPointQueryResult q1, q2;
+        void* a = nullptr;
+        void* b = nullptr;
+        if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &a, 12000, cudaEnableDefault, &q1) ==
+                cudaSuccess &&
+            q1 == cudaDriverEntryPointSuccess &&
+            cudaGetDriverEntryPointByVersion("cuMemGetAddressRange", &b, 12000, cudaEnableDefault, &q2) ==
+                cudaSuccess &&
+            q2 == cudaDriverEntryPointSuccess) {
+            d.wait32 = reinterpret_cast<decltype(&cuStreamWaitValue32)>(a);
+            d.range = reinterpret_cast<decltype(&cuMemGetAddressRange)>(b);
+            d.ok = true;
+        }
+        cudaGetLastError();
+        return d;
+    }();
+    return f;
+}
+
+// pirk_ipc_open mappings: handle bytes -> (base, count), process-wide
+struct IpcMap {
+    std::mutex mu;
+    std::map<std::string, std::pair<void*, int>> by_handle;
+    std::map<void*, std::string> by_base;
+};
+IpcMap& ipc_map() {
+    static IpcMap m;
+    return m;
+}
+}  // namespace
+
+pirk_status pirk_step_window(pirk_ctx* ctx, const pirk_model* m, int32_t method,
+                             const pirk_window* win, const double* p0, const double* p1,
+                             double t, double hk, uint64_t step_index, uint64_t* fail_ptr) {
+    return step_window_impl(ctx, m, method, win, nullptr, nullptr, p0, p1, t, hk, step_index, fail_ptr);
+}
+
+pirk_status pirk_step_window_mirror(pirk_ctx* ctx, const pirk_model* m, int32_t method,
+                                    const pirk_window* win, double* mir0, double* mir1,
+                                    const double* p0, const double* p1, double t, double hk,
+                                    uint64_t step_index, uint64_t* fail_ptr) {
+    if (!mir0 || !mir1) return ctx ? fail(ctx, PIRK_EINVAL, "step_window_mirror: mirror pointers missing")
+                                   : PIRK_EINVAL;
+    return step_window_impl(ctx, m, method, win, mir0, mir1, p0, p1, t, hk, step_index, fail_ptr);
+}
+
+pirk_status pirk_ipc_export(const void* dptr, unsigned char handle[64], uint64_t* offset) {
+    if (!dptr || !handle || !offset) return PIRK_EINVAL;
+    const DriverFns& d = driver_fns();
+    if (!d.ok) return PIRK_ECUDA;
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (d.range(&base, &size, reinterpret_cast<CUdeviceptr>(dptr)) != CUDA_SUCCESS) return PIRK_EINVAL;
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)) != cudaSuccess) {
+        cudaGetLastError();
+        return PIRK_ECUDA;
+    }
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle, &h, 64);
+    *offset = static_cast<uint64_t>(reinterpret_cast<CUdeviceptr>(dptr) - base);
+    return PIRK_OK;
+}
+
+pirk_status pirk_ipc_open(int device, const unsigned char handle[64], void** base) {
+    if (!handle || !base) return PIRK_EINVAL;
+    *base = nullptr;
+    IpcMap& m = ipc_map();
+    std::lock_guard<std::mutex> lk(m.mu);
+    std::string key(reinterpret_cast<const char*>(handle), 64);
+    key += std::to_string(device);
+    auto it = m.by_handle.find(key);
+    if (it != m.by_handle.end()) {
+        it->second.second++;
+        *base = it->second.first;
+        return PIRK_OK;
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return PIRK_ECUDA;
+    }
+    m.by_handle[key] = {p, 1};
+    m.by_base[p] = key;
+    *base = p;
+    return PIRK_OK;
+}
+
+pirk_status pirk_ipc_close(void* base) {
+    if (!base) return PIRK_EINVAL;
+    IpcMap& m = ipc_map();
+    std::lock_guard<std::mutex> lk(m.mu);
+    auto it = m.by_base.find(base);
+    if (it == m.by_base.end()) return PIRK_EINVAL;
+    auto& ent = m.by_handle[it->second];
+    if (--ent.second > 0) return PIRK_OK;
+    m.by_handle.erase(it->second);
+    m.by_base.erase(it);
+    return cudaIpcCloseMemHandle(base) == cudaSuccess ? PIRK_OK : (cudaGetLastError(), PIRK_ECUDA);
+}
+
+pirk_status pirk_wait_flag(pirk_ctx* ctx, const uint32_t* flag, uint32_t value) {
+    if (!ctx || !flag) return PIRK_EINVAL;
+    LOCK(ctx);
+    const DriverFns& d = driver_fns();
+    if (!d.ok) return fail(ctx, PIRK_ECUDA, "wait_flag: driver entry point cuStreamWaitValue32 missing");
+    if (d.wait32(reinterpret_cast<CUstream>(ctx->stream), reinterpret_cast<CUdeviceptr>(flag), value,
+                 CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+        return fail(ctx, PIRK_ECUDA, "wait_flag: cuStreamWaitValue32 failed");
+    return PIRK_OK;
+}
+
+pirk_status pirk_signal_flag(pirk_ctx* ctx, uint32_t* flag, uint32_t value) {
+    if (!ctx || !flag) return PIRK_EINVAL;
+    LOCK(ctx);
+    ctx->launches++;
+    CK(ctx, launch_signal_flag(flag, value, ctx->stream));
     return PIRK_OK;
 }
 

@@ -74,6 +74,15 @@ __global__ void fill_kernel(unsigned long long* p, unsigned long long v, uint64_
         p[i] = v;
 }
 
+// Cross-process step flag (pirk_signal_flag): stream order puts this after the
+// launches that stored halo units into the peer's window; the system-scope
+// fence plus release store make those stores visible to the peer GPU before
+// the flag is.
+__global__ void signal_flag_kernel(unsigned* flag, unsigned v) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+
 static unsigned grid_for(uint64_t n) {
     uint64_t b = (n + 255) / 256;
     if (b > 148ull * 16) b = 148ull * 16;
@@ -107,6 +116,10 @@ cudaError_t launch_center_radius(double* a, double* b, uint64_t n, cudaStream_t 
 cudaError_t launch_fill(unsigned long long* p, unsigned long long v, uint64_t n,
                         cudaStream_t stream) {
     fill_kernel<<<grid_for(n), 256, 0, stream>>>(p, v, n);
+    return cudaGetLastError();
+}
+cudaError_t launch_signal_flag(unsigned* flag, unsigned v, cudaStream_t stream) {
+    signal_flag_kernel<<<1, 1, 0, stream>>>(flag, v);
     return cudaGetLastError();
 }
 

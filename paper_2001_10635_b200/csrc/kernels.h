@@ -119,5 +119,7 @@ cudaError_t launch_center_radius(double* lo_to_c, double* hi_to_r, uint64_t n,
                                  cudaStream_t stream);
 cudaError_t launch_fill(unsigned long long* p, unsigned long long v, uint64_t n,
                         cudaStream_t stream);
+// *flag = v (release, system scope) after all prior work on the stream.
+cudaError_t launch_signal_flag(unsigned* flag, unsigned v, cudaStream_t stream);
 
 }  // namespace pirk

@@ -603,8 +603,11 @@ class Engine:
 def step_window(model: SystemModel, method: str, in0_ptr: int, in1_ptr: int, out0_ptr: int,
                 out1_ptr: int, win_begin: int, win_len: int, out_begin: int, out_end: int,
                 p0: Optional[Sequence[float]], p1: Optional[Sequence[float]], t: float, hk: float,
-                step_index: int, fail_ptr: int = 0, *, ctx: Optional[Context] = None) -> None:
-    """pirk_step_window on caller-owned device buffers (raw pointers)."""
+                step_index: int, fail_ptr: int = 0, *, ctx: Optional[Context] = None,
+                mirror=None) -> None:
+    """pirk_step_window on caller-owned device buffers (raw pointers).  With
+    ``mirror=(m0, m1)`` (pirk_step_window_mirror) every output unit is also
+    stored to m0 / m1, indexed like out0 / out1 (a peer's window)."""
     ctx = ctx or get_context()
     m = model_struct(model)
     w = _lib.PirkWindow(in0_ptr, in1_ptr, out0_ptr, out1_ptr, win_begin, win_len, out_begin,
@@ -612,6 +615,11 @@ def step_window(model: SystemModel, method: str, in0_ptr: int, in1_ptr: int, out
     code = {"mixed-monotonicity": _lib.METHOD_MM, "growth-bound": _lib.METHOD_GB}[method]
     a0 = np.asarray(p0, dtype=np.float64) if p0 is not None else None
     a1 = np.asarray(p1, dtype=np.float64) if p1 is not None else None
-    ctx.check(_lib.lib().pirk_step_window(ctx.handle, C.byref(m), code, C.byref(w),
-                                          _lib.dptr(a0), _lib.dptr(a1), float(t), float(hk),
-                                          int(step_index), C.c_void_p(fail_ptr)))
+    if mirror is None:
+        ctx.check(_lib.lib().pirk_step_window(ctx.handle, C.byref(m), code, C.byref(w),
+                                              _lib.dptr(a0), _lib.dptr(a1), float(t), float(hk),
+                                              int(step_index), C.c_void_p(fail_ptr)))
+    else:
+        ctx.check(_lib.lib().pirk_step_window_mirror(
+            ctx.handle, C.byref(m), code, C.byref(w), C.c_void_p(mirror[0]), C.c_void_p(mirror[1]),
+            _lib.dptr(a0), _lib.dptr(a1), float(t), float(hk), int(step_index), C.c_void_p(fail_ptr)))

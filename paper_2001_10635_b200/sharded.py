@@ -147,6 +147,139 @@ class HaloExchanger:
             dev.copy_(host)
 
 
+class PeerStores:
+    """Halo exchange without a separate transfer, one process per GPU: the
+    launch that computes a rank's 4 boundary units stores them a second time,
+    over NVLink peer memory, straight into the neighbour's window
+    (pirk_step_window_mirror into buffers opened with pirk_ipc_open), then
+    raises the neighbour's step flag (pirk_signal_flag); the neighbour's
+    stream waits for that flag (pirk_wait_flag, cuStreamWaitValue32) before
+    its next boundary launch.  Per step each rank runs
+        wait(neighbour flags >= k-1) | boundary units (+ peer stores) |
+        signal(k) | interior units
+    so a neighbour's next step overlaps this rank's interior.  The flag is
+    also the write-after-read guard: the neighbour's halo for step k is in
+    the buffer its step k-1 read, and its flag k-1 is raised only after its
+    boundary launch (the only reader of the halo) of step k-1.
+
+    Only the control plane (handle exchange, barriers) uses
+    torch.distributed, so it runs over NCCL or gloo alike -- on one GPU
+    several processes test the same path with device-local "peer" stores.
+    Requires K = 1 (halo 4) and every shard at least 8 units wide."""
+
+    def __init__(self, shard: Shard, unit: int, ctx, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.shard = shard
+        self.unit = unit
+        self.ctx = ctx
+        self.group = group
+        self.seq = 0
+        self._bases = []
+        if shard.world > 1 and shard.end - shard.begin < 8:
+            raise ValueError("peer-store halos need at least 8 units per rank")
+
+    # ---- setup -------------------------------------------------------------
+    @staticmethod
+    def _export(t):
+        import ctypes as C
+
+        from . import _lib
+
+        h = C.create_string_buffer(64)
+        off = C.c_uint64(0)
+        st = _lib.lib().pirk_ipc_export(C.c_void_p(t.data_ptr()), h, C.byref(off))
+        if st != _lib.OK:
+            raise RuntimeError(f"pirk_ipc_export failed (status {st})")
+        return h.raw, off.value
+
+    def _open(self, device, handle, offset):
+        import ctypes as C
+
+        from . import _lib
+
+        base = C.c_void_p(0)
+        st = _lib.lib().pirk_ipc_open(int(device), handle, C.byref(base))
+        if st != _lib.OK:
+            raise RuntimeError(f"pirk_ipc_open failed (status {st})")
+        self._bases.append(base.value)
+        return base.value + offset
+
+    def attach(self, run: "ShardedReach"):
+        """Export this rank's window buffers and flags, map the neighbours'.
+        Collective over the group; call after run.alloc()."""
+        import torch
+
+        s = self.shard
+        dev = run.a[0].device
+        self.flags = torch.zeros(2, dtype=torch.int32, device=dev)  # [from left, from right]
+        self.local = [run.a[0], run.a[1], run.b[0], run.b[1]]
+        mine = {"win_begin": s.win_begin, "bufs": [self._export(t) for t in self.local],
+                "flags": self._export(self.flags)}
+        torch.cuda.synchronize(dev)  # flags zeroed before any neighbour can raise them
+        allv = [None] * s.world
+        self.dist.all_gather_object(allv, mine, group=self.group)
+        self.nb = {}
+        for side, r in (("left", s.rank - 1), ("right", s.rank + 1)):
+            if 0 <= r < s.world:
+                o = allv[r]
+                self.nb[side] = {"win_begin": o["win_begin"],
+                                 "bufs": [self._open(dev.index, *b) for b in o["bufs"]],
+                                 "flags": self._open(dev.index, *o["flags"])}
+        self.dist.barrier(group=self.group)
+
+    def close(self):
+        """Unmap the neighbours' buffers once every rank is done with them."""
+        import torch
+
+        from . import _lib
+
+        torch.cuda.synchronize()
+        self.dist.barrier(group=self.group)
+        for b in self._bases:
+            _lib.lib().pirk_ipc_close(b)
+        self._bases = []
+
+    # ---- per step ------------------------------------------------------------
+    def _on_stream(self, fn, ptr: int, value: int):
+        """fn(ctx, ptr, value) on torch's current stream (like device_step_fn)."""
+        import torch
+
+        from . import _lib
+
+        prev = _lib.lib().pirk_get_stream(self.ctx.handle)
+        self.ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+        try:
+            self.ctx.check(fn(self.ctx.handle, ptr, value & 0xFFFFFFFF))
+        finally:
+            self.ctx.set_stream(prev or 0)
+
+    def wait(self, value: int):
+        from . import _lib
+
+        for i, side in enumerate(("left", "right")):
+            if side in self.nb:
+                self._on_stream(_lib.lib().pirk_wait_flag, self.flags.data_ptr() + 4 * i, value)
+
+    def signal(self, value: int):
+        from . import _lib
+
+        # I am the right neighbour of my left neighbour: its flags[1]
+        for side, slot in (("left", 1), ("right", 0)):
+            if side in self.nb:
+                self._on_stream(_lib.lib().pirk_signal_flag, self.nb[side]["flags"] + 4 * slot, value)
+
+    def mirror(self, side: str, out0, out_begin: int):
+        """(m0, m1): the neighbour's output buffers at unit out_begin -- the
+        buffer with the same role (A or B) as this rank's out0, since all ranks
+        swap in lockstep."""
+        idx = [t.data_ptr() for t in self.local].index(out0.data_ptr())
+        nb = self.nb[side]
+        off = (out_begin - nb["win_begin"]) * self.unit * 8
+        return nb["bufs"][idx] + off, nb["bufs"][idx + 1] + off
+
+
 def device_step_fn(model: SystemModel, method: str, ctx=None):
     """Windowed RK4 step on the B200 (pirk_step_window on torch tensors), on
     torch's current stream; the context's own stream is restored afterwards."""
@@ -156,7 +289,7 @@ def device_step_fn(model: SystemModel, method: str, ctx=None):
     ctx = ctx or get_context()
 
     def step(in0, in1, out0, out1, win_begin, win_len, out_begin, out_end, p0, p1, t, hk, k,
-             fail_ptr=0):
+             fail_ptr=0, mirror=None):
         import torch
 
         prev = _lib.lib().pirk_get_stream(ctx.handle)
@@ -167,7 +300,7 @@ def device_step_fn(model: SystemModel, method: str, ctx=None):
             off = (out_begin - win_begin) * unit * 8
             step_window(model, method, in0.data_ptr(), in1.data_ptr(), out0.data_ptr() + off,
                         out1.data_ptr() + off, win_begin, win_len, out_begin, out_end, p0, p1, t,
-                        hk, k, fail_ptr, ctx=ctx)
+                        hk, k, fail_ptr, ctx=ctx, mirror=mirror)
         finally:
             ctx.set_stream(prev or 0)
     return step
@@ -256,6 +389,8 @@ class ShardedReach:
         units are computed; the units next to the window edges follow once
         the halos have landed.  Every unit is still computed once, from the
         same inputs, so results do not depend on ``overlap``."""
+        if isinstance(self.ex, PeerStores):
+            return self._run_peer(steps, k0)
         s = self.shard
         fp = self._fail_ptr()
         for i, (t, hk) in enumerate(steps):
@@ -280,6 +415,29 @@ class ShardedReach:
             self.step_fn(self.a[0], self.a[1], self.b[0], self.b[1], *args, lo, hi, self.p0, self.p1, t,
                          hk, k0 + i, fp)
             self.a, self.b = self.b, self.a
+
+    def _run_peer(self, steps, k0: int):
+        """Boundary units first, stored into the neighbours' windows by the
+        same launch; then the interior (see PeerStores)."""
+        s, ex = self.shard, self.ex
+        assert self.K == 1, "peer-store halos exchange every step (K = 1)"
+        fp = self._fail_ptr()
+        args = (s.win_begin, s.win_len)
+        has_l, has_r = "left" in ex.nb, "right" in ex.nb
+        ilo = s.begin + 4 if has_l else s.begin
+        ihi = s.end - 4 if has_r else s.end
+        for i, (t, hk) in enumerate(steps):
+            ex.seq += 1
+            ex.wait(ex.seq - 1)
+            a, b = self.a, self.b
+            for side, (blo, bhi) in (("left", (s.begin, s.begin + 4)), ("right", (s.end - 4, s.end))):
+                if side in ex.nb:
+                    self.step_fn(a[0], a[1], b[0], b[1], *args, blo, bhi, self.p0, self.p1, t, hk, k0 + i,
+                                 fp, mirror=ex.mirror(side, b[0], blo))
+            ex.signal(ex.seq)
+            if ilo < ihi:
+                self.step_fn(a[0], a[1], b[0], b[1], *args, ilo, ihi, self.p0, self.p1, t, hk, k0 + i, fp)
+            self.a, self.b = b, a
 
     def owned(self):
         s = self.shard

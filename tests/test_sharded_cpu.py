@@ -187,3 +187,90 @@ def test_bench_gpus_flag_launches_n_ranks():
     r2 = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--launcher-check"],
                         cwd=root, env=env2, capture_output=True, text=True, timeout=120)
     assert r2.returncode != 0 and "WORLD_SIZE=3" in r2.stderr
+
+
+class _LockstepPeers(S.PeerStores):
+    """PeerStores with the transport replaced for a one-process CPU check of
+    ShardedReach._run_peer: "peer memory" is the neighbour rank's window tensor
+    (a view), flags are recorded.  Ranks are stepped one after another per RK4
+    step, which is an order the real flags allow."""
+
+    def __init__(self, shard, unit):
+        self.shard, self.unit, self.seq = shard, unit, 0
+        self.waits, self.signals = [], []
+
+    def link(self, runs):
+        s = self.shard
+        self.local = [runs[s.rank].a[0], runs[s.rank].a[1], runs[s.rank].b[0], runs[s.rank].b[1]]
+        self.nb = {}
+        for side, r in (("left", s.rank - 1), ("right", s.rank + 1)):
+            if 0 <= r < s.world:
+                o = runs[r]
+                self.nb[side] = {"win_begin": o.shard.win_begin, "bufs": [o.a[0], o.a[1], o.b[0], o.b[1]]}
+
+    def wait(self, value):
+        self.waits.append(value)
+
+    def signal(self, value):
+        self.signals.append(value)
+
+    def mirror(self, side, out0, out_begin):
+        idx = [t.data_ptr() for t in self.local].index(out0.data_ptr())
+        nb = self.nb[side]
+        off = (out_begin - nb["win_begin"]) * self.unit
+        return nb["bufs"][idx][off:], nb["bufs"][idx + 1][off:]
+
+
+@pytest.mark.parametrize("kind,world", [("traffic", 2), ("traffic", 3), ("chain", 4), ("heat", 2),
+                                        ("heat", 3), ("traffic_gb", 2)])
+def test_peer_store_schedule_equals_single(kind, world):
+    """The peer-store schedule (boundary units first, stored into the
+    neighbours' windows, then the interior) with the oracle's windowed step,
+    which reads NaN outside its window: bit-identical to one process, and the
+    flag protocol waits for k-1 before raising k on every step."""
+    m, method, lo, hi, plo, phi, t0, t1, h = problem(kind)
+    units, unit = S.units_of(m)
+    if method == "growth-bound":
+        f0, f1 = 0.5 * (hi + lo), 0.5 * (hi - lo)
+        p0, p1 = [0.5 * (phi[0] + plo[0])], [0.5 * (phi[0] - plo[0])]
+    else:
+        f0, f1, p0, p1 = lo, hi, plo, phi
+    base = oracle_step_fn(m, method)
+
+    def step(in0, in1, out0, out1, wb, wl, lo_, hi_, p0_, p1_, t, hk, k, fail_ptr=0, mirror=None):
+        base(in0, in1, out0, out1, wb, wl, lo_, hi_, p0_, p1_, t, hk, k)
+        if mirror is not None:
+            a, n = (lo_ - wb) * unit, (hi_ - lo_) * unit
+            mirror[0][:n] = out0[a:a + n]
+            mirror[1][:n] = out1[a:a + n]
+
+    runs, exs = [], []
+    for r in range(world):
+        shard = S.Shard(units, world, r, 4)
+        ex = _LockstepPeers(shard, unit)
+        run = S.ShardedReach(m, method, shard, step, ex, p0, p1, K=1)
+        a = run.alloc(lambda n: torch.full((n,), float("nan"), dtype=torch.float64))
+        sl = slice(shard.win_begin * unit, shard.win_end * unit)
+        a[0].copy_(torch.from_numpy(np.ascontiguousarray(f0[sl])))
+        a[1].copy_(torch.from_numpy(np.ascontiguousarray(f1[sl])))
+        # halos of the second buffer stay NaN: only peer stores may fill them
+        runs.append(run)
+        exs.append(ex)
+    for ex in exs:
+        ex.link(runs)
+    plan = S.plan_rk4_steps(t0, t1, h)
+    for k, st in enumerate(plan):
+        for run in runs:
+            run.run([st], k)
+    got0 = np.concatenate([run.owned()[0].numpy() for run in runs])
+    got1 = np.concatenate([run.owned()[1].numpy() for run in runs])
+    meth = 0 if method == "mixed-monotonicity" else 1
+    # single-process reference: the same oracle step over the whole state
+    a0, a1 = f0.copy(), f1.copy()
+    for t, hk in plan:
+        a0, a1 = O.step_window(m, meth, a0, a1, 0, units, 0, units, p0, p1, t, hk)
+    np.testing.assert_array_equal(got0, a0)
+    np.testing.assert_array_equal(got1, a1)
+    for ex in exs:
+        assert ex.waits == list(range(len(plan)))
+        assert ex.signals == list(range(1, len(plan) + 1))
