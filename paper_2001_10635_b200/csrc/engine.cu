@@ -662,6 +662,9 @@ struct StreamGuard {
     ~StreamGuard() { if (s) cudaStreamDestroy(s); }
 };
 struct EventGuard {
+    EventGuard() = default;
+    EventGuard(const EventGuard&) = delete;
+    EventGuard& operator=(const EventGuard&) = delete;
     cudaEvent_t e = nullptr;
     ~EventGuard() { if (e) cudaEventDestroy(e); }
 };
@@ -673,15 +676,52 @@ bool heat_single_field_ok() {
     return !v || std::strcmp(v, "strip") == 0;
 }
 
+// Fronts of the skewed ("wavefront") schedule of one field in the
+// field-pipelined driver.  Round r advances step k (state k -> k+1) over the
+// z-planes [front(r-1) - 4k, front(r) - 4k), clamped to [0, U); the last front
+// U + 4(K-1) completes every step.  Field 0 grows its front geometrically from
+// S planes, so integration starts once the first S+4 planes are on the device
+// (not the whole 33 GB field); field 1 ends with rounds of S planes, so its
+// final box leaves the device S planes at a time while the rest integrates.
+// PIRK_SKEW=0: one round (full-field launches); PIRK_SKEW_S: S.
+std::vector<uint64_t> skew_fronts(int field, uint64_t U, uint64_t K) {
+    const uint64_t F = U + 4 * (K - 1);
+    static const long long skew_s = [] {
+        const char* v = std::getenv("PIRK_SKEW");
+        if (v && std::strcmp(v, "0") == 0) return -1ll;
+        const char* sv = std::getenv("PIRK_SKEW_S");
+        return sv ? std::atoll(sv) : 0ll;
+    }();
+    std::vector<uint64_t> fr;
+    if (skew_s < 0) return {F};
+    const uint64_t S = skew_s > 0 ? static_cast<uint64_t>(skew_s) : std::max<uint64_t>(64, (U / 8 + 3) & ~3ull);
+    if (field == 0) {
+        for (uint64_t P = S; P < F; P *= 2) fr.push_back(P);
+    } else {
+        const uint64_t J = 3;
+        for (uint64_t j = J; j >= 1; --j)
+            if (F > j * S && F - j * S > (fr.empty() ? 0 : fr.back())) fr.push_back(F - j * S);
+    }
+    fr.push_back(F);
+    return fr;
+}
+
 // heat3d CTMM recording only the final box (tube_stride 0).  The embedding's
 // halves are independent (cooperative decomposition, models.cpp:20-27, and the
-// heat field reads no input), so the lower field is uploaded, integrated and
-// downloaded while the upper field's transfers overlap it on a copy stream:
-//   copy:    H2D lo | H2D hi, box check |            | D2H lo
-//   compute:        | steps lo          | steps hi   | order check, D2H hi
-// Same kernels, same per-unit arithmetic and failure keys (the field-1 keys
-// carry +n as in the two-field launch), so results and error reports are those
-// of run_large; only PCIe time hides behind the integration.
+// heat field reads no input), so each field is integrated on its own, and the
+// PCIe transfers hide behind the integration:
+//   h2d:     lo (in slabs) | hi, box check
+//   compute:   steps lo (skewed rounds)  | steps hi (skewed tail) | order check
+//   d2h:           final planes of lo as rounds finish  | of hi ...
+// Within a field the rounds of skew_fronts() let integration start on the
+// first planes of the lower field while the rest uploads, and let the upper
+// field's final planes download while its last planes integrate.  Every
+// plane's state k+1 is computed by the same kernel from the same state-k
+// planes as in a full-field launch (step k of round r reads state k on
+// [lo - 4, hi + 4): computed by step k-1 of this round, and not yet
+// overwritten by step k+1, whose front lags by 4 planes), so results and
+// failure keys (field-1 keys carry +n as in the two-field launch) are those of
+// run_large.
 pirk_status run_heat_mm_pipelined(pirk_ctx* ctx, const pirk_model* m, const pirk_problem* p,
                                   pirk_tube* tube, pirk_report* rep) {
     const auto t_setup = Clock::now();
@@ -707,6 +747,7 @@ pirk_status run_heat_mm_pipelined(pirk_ctx* ctx, const pirk_model* m, const pirk
         return fail(ctx, PIRK_EINVAL, "dimension exceeds the device failure-key range");
     e.hm = heat_model(m, PIRK_METHOD_MM);
     const size_t n = e.n;
+    const uint64_t U = e.units, K = e.plan.total, unit = e.unit;
     const bool cache = state_cache_on();
     CK(ctx, cache ? e.a0.alloc_state(ctx, n) : e.a0.alloc(ctx, n));
     CK(ctx, cache ? e.a1.alloc_state(ctx, n) : e.a1.alloc(ctx, n));
@@ -715,51 +756,81 @@ pirk_status run_heat_mm_pipelined(pirk_ctx* ctx, const pirk_model* m, const pirk
     CK(ctx, e.d_fail.alloc(ctx, 2));
     DevBuf<unsigned long long> flag;  // [0] box check, [1] order check
     CK(ctx, flag.alloc(ctx, 2));
-    StreamGuard xs;
+    StreamGuard xs, ds;  // host->device, device->host
     CK(ctx, cudaStreamCreateWithFlags(&xs.s, cudaStreamNonBlocking));
-    EventGuard ev_h0, ev_h1, ev_c0, ev_x;
-    for (EventGuard* g : {&ev_h0, &ev_h1, &ev_c0, &ev_x})
-        CK(ctx, cudaEventCreateWithFlags(&g->e, cudaEventDisableTiming));
+    CK(ctx, cudaStreamCreateWithFlags(&ds.s, cudaStreamNonBlocking));
+    const std::vector<uint64_t> fronts[2] = {skew_fronts(0, U, K), skew_fronts(1, U, K)};
+    std::vector<EventGuard> ev_up(fronts[0].size() + 1), ev_done(fronts[0].size() + fronts[1].size());
+    EventGuard ev_x;
+    for (EventGuard& g : ev_up) CK(ctx, cudaEventCreateWithFlags(&g.e, cudaEventDisableTiming));
+    for (EventGuard& g : ev_done) CK(ctx, cudaEventCreateWithFlags(&g.e, cudaEventDisableTiming));
+    CK(ctx, cudaEventCreateWithFlags(&ev_x.e, cudaEventDisableTiming));
     cudaStream_t cs = ctx->stream;
     CK(ctx, cudaMemsetAsync(e.d_fail.p, 0xff, 2 * sizeof(unsigned long long), cs));
     CK(ctx, cudaMemsetAsync(flag.p, 0xff, 2 * sizeof(unsigned long long), cs));
     mark("allocated");
     CK(ctx, cudaEventRecord(ev_x.e, cs));
     CK(ctx, cudaStreamWaitEvent(xs.s, ev_x.e, 0));
-    CK(ctx, cudaMemcpyAsync(e.a0.p, p->init_lower, n * sizeof(double), cudaMemcpyHostToDevice, xs.s));
-    CK(ctx, cudaEventRecord(ev_h0.e, xs.s));
+    CK(ctx, cudaStreamWaitEvent(ds.s, ev_x.e, 0));
+    // lower field in slabs: round r of field 0 needs planes [0, front_r + 4)
+    uint64_t up = 0;
+    for (size_t r = 0; r < fronts[0].size(); ++r) {
+        const uint64_t end = std::min<uint64_t>(U, fronts[0][r] + 4);
+        if (end > up) {
+            CK(ctx, cudaMemcpyAsync(e.a0.p + up * unit, p->init_lower + up * unit, (end - up) * unit * sizeof(double),
+                                    cudaMemcpyHostToDevice, xs.s));
+            up = end;
+        }
+        CK(ctx, cudaEventRecord(ev_up[r].e, xs.s));
+    }
     CK(ctx, cudaMemcpyAsync(e.a1.p, p->init_upper, n * sizeof(double), cudaMemcpyHostToDevice, xs.s));
     CK(ctx, launch_box_check(e.a0.p, e.a1.p, n, flag.p, xs.s));  // interval.cpp:14-22
     ctx->launches++;
-    CK(ctx, cudaEventRecord(ev_h1.e, xs.s));
+    CK(ctx, cudaEventRecord(ev_up.back().e, xs.s));
     mark("uploads enqueued");
     const double setup_s = since(t_setup);
 
     const auto t_int = Clock::now();
     double* fin[2] = {nullptr, nullptr};
+    size_t ne = 0;
+    auto clampU = [&](uint64_t P, uint64_t k) -> uint64_t {
+        const uint64_t d = 4 * k;
+        return P <= d ? 0 : std::min<uint64_t>(U, P - d);
+    };
     for (int f = 0; f < 2; ++f) {
-        CK(ctx, cudaStreamWaitEvent(cs, f == 0 ? ev_h0.e : ev_h1.e, 0));
-        double* a = f == 0 ? e.a0.p : e.a1.p;
-        double* b = f == 0 ? e.b0.p : e.b1.p;
-        for (uint64_t k = 0; k < e.plan.total; ++k) {
-            const StepConsts sc = host_step(e.t0, e.t1, e.h, k, e.plan.total);
-            WindowArgs w = f == 0 ? WindowArgs{a, a, b, b, 0, e.units, 0, e.units}
-                                  : WindowArgs{a, a, b, b, 0, e.units, 0, e.units};
-            ctx->launches++;
-            CK(ctx, exact_mode(ctx) ? launch_heat_step<true>(e.hm, w, sc, k, e.d_fail.p, cs, f)
-                                    : launch_heat_step<false>(e.hm, w, sc, k, e.d_fail.p, cs, f));
-            std::swap(a, b);
-        }
-        fin[f] = a;
-        if (f == 0) {  // the lower field's box leaves while the upper one integrates
-            CK(ctx, cudaEventRecord(ev_c0.e, cs));
-            CK(ctx, cudaStreamWaitEvent(xs.s, ev_c0.e, 0));
-            CK(ctx, cudaMemcpyAsync(tube->lower, fin[0], n * sizeof(double), cudaMemcpyDeviceToHost, xs.s));
+        double* buf[2] = {f == 0 ? e.a0.p : e.a1.p, f == 0 ? e.b0.p : e.b1.p};
+        fin[f] = buf[K % 2];
+        double* host = f == 0 ? tube->lower : tube->upper;
+        uint64_t prev = 0;
+        for (size_t r = 0; r < fronts[f].size(); ++r) {
+            const uint64_t P = fronts[f][r];
+            if (f == 0) CK(ctx, cudaStreamWaitEvent(cs, ev_up[r].e, 0));
+            else if (r == 0) CK(ctx, cudaStreamWaitEvent(cs, ev_up.back().e, 0));
+            for (uint64_t k = 0; k < K; ++k) {
+                const uint64_t lo = clampU(prev, k), hi = clampU(P, k);
+                if (lo >= hi) continue;
+                const StepConsts sc = host_step(e.t0, e.t1, e.h, k, K);
+                double* in = buf[k % 2];
+                double* out = buf[(k + 1) % 2] + lo * unit;
+                WindowArgs w{in, in, out, out, 0, U, lo, hi};
+                ctx->launches++;
+                CK(ctx, exact_mode(ctx) ? launch_heat_step<true>(e.hm, w, sc, k, e.d_fail.p, cs, f)
+                                        : launch_heat_step<false>(e.hm, w, sc, k, e.d_fail.p, cs, f));
+            }
+            // planes whose last step ran in this round leave the device now
+            const uint64_t flo = clampU(prev, K - 1), fhi = clampU(P, K - 1);
+            if (flo < fhi) {
+                CK(ctx, cudaEventRecord(ev_done[ne].e, cs));
+                CK(ctx, cudaStreamWaitEvent(ds.s, ev_done[ne].e, 0));
+                ++ne;
+                CK(ctx, cudaMemcpyAsync(host + flo * unit, fin[f] + flo * unit, (fhi - flo) * unit * sizeof(double),
+                                        cudaMemcpyDeviceToHost, ds.s));
+            }
+            prev = P;
         }
     }
     CK(ctx, launch_order_check(fin[0], fin[1], n, flag.p + 1, cs));  // reach.cpp:181-186
     ctx->launches++;
-    CK(ctx, cudaMemcpyAsync(tube->upper, fin[1], n * sizeof(double), cudaMemcpyDeviceToHost, cs));
     unsigned long long hf[4];
     CK(ctx, cudaMemcpyAsync(hf, e.d_fail.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs));
     CK(ctx, cudaMemcpyAsync(hf + 2, flag.p, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, cs));
@@ -767,7 +838,8 @@ pirk_status run_heat_mm_pipelined(pirk_ctx* ctx, const pirk_model* m, const pirk
     CK(ctx, cudaStreamSynchronize(cs));
     mark("compute stream done");
     CK(ctx, cudaStreamSynchronize(xs.s));
-    mark("copy stream done");
+    CK(ctx, cudaStreamSynchronize(ds.s));
+    mark("copy streams done");
     const double integ_s = since(t_int);
 
     if (hf[2] != kNoFail) {  // the box is validated before anything else (interval.cpp:14-22)

@@ -579,6 +579,55 @@ def test_heat_pipelined_final_box(mode):
         c.close()
 
 
+_SKEW_CHILD = r"""
+import sys, numpy as np, paper_2001_10635_b200 as pk
+g, steps, out = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
+n = g ** 3
+rng = np.random.default_rng(5)
+lo = rng.uniform(0.5, 1.0, n)
+hi = lo + rng.uniform(0.0, 0.5, n)
+h = 0.2 / (g - 1) ** 2
+m = pk.make_heat3d(g)
+prob = pk.ReachProblem(m, pk.IntervalVector(lo, hi), None, 0.0, steps * h, h, 0)
+c = pk.Context(0, "fast")
+t = pk.mixed_monotonicity(prob, ctx=c)
+np.save(out + "_lo.npy", t.lower[-1]); np.save(out + "_hi.npy", t.upper[-1])
+"""
+
+
+def test_heat_pipelined_skew_schedules_identical(tmp_path):
+    """The field-pipelined driver's skewed rounds (engine.cu skew_fronts:
+    strips of S planes, lower field started before its upload completes,
+    upper field downloaded S planes at a time) give bit-identical boxes for any
+    strip width, including the unskewed schedule (PIRK_SKEW=0) and strips
+    narrower than the 4-plane step cone, and stay within the fast-mode
+    tolerance of the oracle."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    g, steps = 162, 24  # n = 4.25e6 >= 2^22; 24 steps: the step cone spans 92 planes
+    res = {}
+    for name, env in (("noskew", {"PIRK_SKEW": "0"}), ("s8", {"PIRK_SKEW_S": "8"}),
+                      ("s3", {"PIRK_SKEW_S": "3"}), ("s40", {"PIRK_SKEW_S": "40"}), ("default", {})):
+        out = str(tmp_path / name)
+        r = subprocess.run([sys.executable, "-c", _SKEW_CHILD, str(g), str(steps), out],
+                           env=dict(os.environ, **env), cwd=root, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        res[name] = (np.load(out + "_lo.npy"), np.load(out + "_hi.npy"))
+    for name in res:
+        assert np.array_equal(res[name][0], res["noskew"][0]), name
+        assert np.array_equal(res[name][1], res["noskew"][1]), name
+    n = g ** 3
+    rng = np.random.default_rng(5)
+    lo = rng.uniform(0.5, 1.0, n)
+    hi = lo + rng.uniform(0.0, 0.5, n)
+    h = 0.2 / (g - 1) ** 2
+    m, prob = heat_problem(g, t1=steps * h, h=h, stride=0, lo=lo, hi=hi)
+    ref = oracle_for("mm", prob)
+    for f, r in ((0, ref.lower[-1]), (1, ref.upper[-1])):
+        got = res["default"][f]
+        assert np.max(np.abs(got - r) / np.abs(r)) <= 1e-12
+
+
 def test_small_serial_kernel_variant():
     """The one-thread small-system integrator (PIRK_SMALL_SERIAL=1) and the
     default warp-parallel one give the same results: the small-system tests
