@@ -302,7 +302,9 @@ def heat_e2e(args, pk, torch, world):
            "d2h_bytes_per_step": 2 * n * 8, "seconds": dt, "rk4_steps": steps,
            "n": n, "grid": g, "api": "paper_2001_10635_b200.mixed_monotonicity",
            "step": "one full C5 reach call (H2D initial box, 100 RK4 steps, order check, D2H final box); "
-                   "lower field integrated while the upper field uploads, downloaded while it integrates",
+                   "lower field integrated while the upper field uploads, downloaded while it integrates; "
+                   "skewed rounds start the lower field on its first uploaded planes and send the upper "
+                   "field's final planes back in strips (engine.cu skew_fronts)",
            "warmup_calls": 1, "state_cache": "warm (the 4 state buffers kept by the previous call)",
            "cold": {"value": 2.0 * n * cold.report.steps / dt_cold, "seconds": dt_cold,
                     "state_cache": "cold (release_cache() before the call: cudaMalloc of the state inside)"},

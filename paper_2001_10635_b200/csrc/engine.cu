@@ -679,26 +679,34 @@ bool heat_single_field_ok() {
 // Fronts of the skewed ("wavefront") schedule of one field in the
 // field-pipelined driver.  Round r advances step k (state k -> k+1) over the
 // z-planes [front(r-1) - 4k, front(r) - 4k), clamped to [0, U); the last front
-// U + 4(K-1) completes every step.  Field 0 grows its front geometrically from
-// S planes, so integration starts once the first S+4 planes are on the device
-// (not the whole 33 GB field); field 1 ends with rounds of S planes, so its
-// final box leaves the device S planes at a time while the rest integrates.
-// PIRK_SKEW=0: one round (full-field launches); PIRK_SKEW_S: S.
+// F = U + 4(K-1) completes every step.  Field 0 starts with a front of S0
+// planes and doubles it while it stays within U/2, then completes: integration
+// starts once the first S0+4 planes are on the device (not the whole 33 GB
+// field) and the completing round still runs wide strips.  Field 1 completes
+// in J tail rounds of S planes, so its final box leaves the device S planes at
+// a time while the rest integrates.  Narrow strips cost wave quantisation and
+// pipeline fill per launch, so S trades that against the exposed first upload
+// and last download.  PIRK_SKEW=0: one round (full-field launches);
+// PIRK_SKEW_S / _S0 / _J override S, S0, J (A/B).
 std::vector<uint64_t> skew_fronts(int field, uint64_t U, uint64_t K) {
     const uint64_t F = U + 4 * (K - 1);
-    static const long long skew_s = [] {
+    auto env = [](const char* name) -> long long {
+        const char* v = std::getenv(name);
+        return v ? std::atoll(v) : 0ll;
+    };
+    static const bool off = [] {
         const char* v = std::getenv("PIRK_SKEW");
-        if (v && std::strcmp(v, "0") == 0) return -1ll;
-        const char* sv = std::getenv("PIRK_SKEW_S");
-        return sv ? std::atoll(sv) : 0ll;
+        return v && std::strcmp(v, "0") == 0;
     }();
+    static const long long s_env = env("PIRK_SKEW_S"), s0_env = env("PIRK_SKEW_S0"), j_env = env("PIRK_SKEW_J");
+    if (off) return {F};
+    const uint64_t S = s_env > 0 ? static_cast<uint64_t>(s_env) : std::max<uint64_t>(64, (U / 8 + 3) & ~3ull);
+    const uint64_t S0 = s0_env > 0 ? static_cast<uint64_t>(s0_env) : S;
+    const uint64_t J = j_env > 0 ? static_cast<uint64_t>(j_env) : 3;
     std::vector<uint64_t> fr;
-    if (skew_s < 0) return {F};
-    const uint64_t S = skew_s > 0 ? static_cast<uint64_t>(skew_s) : std::max<uint64_t>(64, (U / 8 + 3) & ~3ull);
     if (field == 0) {
-        for (uint64_t P = S; P < F; P *= 2) fr.push_back(P);
+        for (uint64_t P = S0; P < F && (fr.empty() || P <= U / 2); P *= 2) fr.push_back(P);
     } else {
-        const uint64_t J = 3;
         for (uint64_t j = J; j >= 1; --j)
             if (F > j * S && F - j * S > (fr.empty() ? 0 : fr.back())) fr.push_back(F - j * S);
     }

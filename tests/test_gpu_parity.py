@@ -591,7 +591,7 @@ m = pk.make_heat3d(g)
 prob = pk.ReachProblem(m, pk.IntervalVector(lo, hi), None, 0.0, steps * h, h, 0)
 c = pk.Context(0, "fast")
 t = pk.mixed_monotonicity(prob, ctx=c)
-np.save(out + "_lo.npy", t.lower[-1]); np.save(out + "_hi.npy", t.upper[-1])
+np.save(out + "_lo.npy", t.entries[-1].box.lower); np.save(out + "_hi.npy", t.entries[-1].box.upper)
 """
 
 
@@ -607,7 +607,8 @@ def test_heat_pipelined_skew_schedules_identical(tmp_path):
     g, steps = 162, 24  # n = 4.25e6 >= 2^22; 24 steps: the step cone spans 92 planes
     res = {}
     for name, env in (("noskew", {"PIRK_SKEW": "0"}), ("s8", {"PIRK_SKEW_S": "8"}),
-                      ("s3", {"PIRK_SKEW_S": "3"}), ("s40", {"PIRK_SKEW_S": "40"}), ("default", {})):
+                      ("s3", {"PIRK_SKEW_S": "3", "PIRK_SKEW_S0": "5", "PIRK_SKEW_J": "7"}),
+                      ("s40", {"PIRK_SKEW_S": "40", "PIRK_SKEW_J": "1"}), ("default", {})):
         out = str(tmp_path / name)
         r = subprocess.run([sys.executable, "-c", _SKEW_CHILD, str(g), str(steps), out],
                            env=dict(os.environ, **env), cwd=root, capture_output=True, text=True, timeout=600)
