@@ -294,9 +294,12 @@ pirk_status pirk_step_window(pirk_ctx* ctx, const pirk_model* model, int32_t met
  * window over NVLink and then raises the neighbour's step flag; the
  * neighbour's stream waits for the flag before its next boundary launch.
  *
- * pirk_step_window_mirror: pirk_step_window that stores every output unit a
- *   second time, to mir0 / mir1 (indexed like out0 / out1: mir0[0] is unit
- *   out_begin; typically a peer process's window opened with pirk_ipc_open).
+ * pirk_step_window_mirror: pirk_step_window that also stores output units
+ *   into the neighbours' windows (typically a peer process's buffers opened
+ *   with pirk_ipc_open): unit u (u < lo_end) also to lo0/lo1[u - out_begin],
+ *   unit u (u >= hi_begin) also to hi0/hi1[u - out_begin].  NULL lo0 / hi0
+ *   disables that side.  One launch over a rank's whole slab with lo_end =
+ *   out_begin + 4 and hi_begin = out_end - 4 computes and sends its halos.
  * pirk_ipc_export: IPC handle (64 bytes) of the allocation holding dptr and the
  *   byte offset of dptr inside it (dptr may be a sub-allocation, e.g. torch's).
  * pirk_ipc_open: map a peer process's allocation on `device`; returns its base
@@ -306,8 +309,16 @@ pirk_status pirk_step_window(pirk_ctx* ctx, const pirk_model* model, int32_t met
  *   flag is a uint32 in this process's device memory.
  * pirk_signal_flag: after all prior work on the ctx stream, *flag = value
  *   (system-scope release; flag may be a peer process's memory). */
+typedef struct pirk_mirror {
+    double* lo0;
+    double* lo1;
+    uint64_t lo_end;
+    double* hi0;
+    double* hi1;
+    uint64_t hi_begin;
+} pirk_mirror;
 pirk_status pirk_step_window_mirror(pirk_ctx* ctx, const pirk_model* model, int32_t method,
-                                    const pirk_window* win, double* mir0, double* mir1,
+                                    const pirk_window* win, const pirk_mirror* mirror,
                                     const double* p0, const double* p1, double t, double hk,
                                     uint64_t step_index, uint64_t* fail);
 pirk_status pirk_ipc_export(const void* dptr, unsigned char handle[64], uint64_t* offset);

@@ -99,6 +99,19 @@ class PirkWindow(C.Structure):
     ]
 
 
+class PirkMirror(C.Structure):
+    """pirk_mirror (include/pirk_c.h): units < lo_end also to lo0/lo1, units
+    >= hi_begin also to hi0/hi1 (indexed from out_begin)."""
+    _fields_ = [
+        ("lo0", C.c_void_p),
+        ("lo1", C.c_void_p),
+        ("lo_end", C.c_uint64),
+        ("hi0", C.c_void_p),
+        ("hi1", C.c_void_p),
+        ("hi_begin", C.c_uint64),
+    ]
+
+
 # Every symbol include/pirk_c.h declares, with its ctypes signature.
 _MP = C.POINTER(PirkModel)
 _PP = C.POINTER(PirkProblem)
@@ -144,7 +157,7 @@ SIGNATURES = {
     "pirk_step_window": (C.c_int, [C.c_void_p, _MP, C.c_int32, C.POINTER(PirkWindow), _DP, _DP,
                                    C.c_double, C.c_double, C.c_uint64, C.c_void_p]),
     "pirk_step_window_mirror": (C.c_int, [C.c_void_p, _MP, C.c_int32, C.POINTER(PirkWindow),
-                                          C.c_void_p, C.c_void_p, _DP, _DP, C.c_double, C.c_double,
+                                          C.POINTER(PirkMirror), _DP, _DP, C.c_double, C.c_double,
                                           C.c_uint64, C.c_void_p]),
     "pirk_ipc_export": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_uint64)]),
     "pirk_ipc_open": (C.c_int, [C.c_int, C.c_char_p, C.POINTER(C.c_void_p)]),

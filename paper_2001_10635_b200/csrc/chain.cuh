@@ -449,9 +449,14 @@ chain_warp_kernel(const ChainModel m, const WindowArgs w, const StepConstsN scs,
         const long long o = g - static_cast<long long>(w.out_begin);
         w.out0[o] = x0[k];
         w.out1[o] = x1[k];
-        if (w.mir0) {  // boundary launch of a lane: the neighbour's halo, over peer memory
+        // units the neighbours need as halo: also into their windows, over peer memory
+        if (w.mir0 && static_cast<uint64_t>(g) < w.mir_lo_end) {
             w.mir0[o] = x0[k];
             w.mir1[o] = x1[k];
+        }
+        if (w.mirh0 && static_cast<uint64_t>(g) >= w.mir_hi_begin) {
+            w.mirh0[o] = x0[k];
+            w.mirh1[o] = x1[k];
         }
         if (!finite_d(x0[k]) || !finite_d(x1[k])) flag(k, step + S - 1);
     }

@@ -2079,7 +2079,7 @@ void pirk_engine_destroy(pirk_engine* e) {
 
 namespace {
 pirk_status step_window_impl(pirk_ctx* ctx, const pirk_model* m, int32_t method, const pirk_window* win,
-                             double* mir0, double* mir1, const double* p0, const double* p1, double t,
+                             const pirk_mirror* mir, const double* p0, const double* p1, double t,
                              double hk, uint64_t step_index, uint64_t* fail_ptr) {
     if (!ctx || !win) return PIRK_EINVAL;
     LOCK(ctx);
@@ -2109,11 +2109,21 @@ pirk_status step_window_impl(pirk_ctx* ctx, const pirk_model* m, int32_t method,
     sc.h6 = hk / 6.0;
     const ChainModel cm = chain_model(m, method, q0, q1);
     const HeatModel hm = heat_model(m, method);
-    if ((mir0 == nullptr) != (mir1 == nullptr))
-        return fail(ctx, PIRK_EINVAL, "step_window: mirror needs both fields");
     WindowArgs w{win->in0, win->in1, win->out0, win->out1, wb, we, win->out_begin, win->out_end};
-    w.mir0 = mir0;
-    w.mir1 = mir1;
+    if (mir) {
+        if ((mir->lo0 == nullptr) != (mir->lo1 == nullptr) || (mir->hi0 == nullptr) != (mir->hi1 == nullptr))
+            return fail(ctx, PIRK_EINVAL, "step_window_mirror: a mirror side needs both fields");
+        if (mir->lo0) {
+            w.mir0 = mir->lo0;
+            w.mir1 = mir->lo1;
+            w.mir_lo_end = mir->lo_end;
+        }
+        if (mir->hi0) {
+            w.mirh0 = mir->hi0;
+            w.mirh1 = mir->hi1;
+            w.mir_hi_begin = mir->hi_begin;
+        }
+    }
     CK(ctx, step_launch(ctx, ctx->stream, m, cm, hm, w, sc, step_index,
                         reinterpret_cast<unsigned long long*>(fail_ptr)));
     return PIRK_OK;
@@ -2162,16 +2172,15 @@ IpcMap& ipc_map() {
 pirk_status pirk_step_window(pirk_ctx* ctx, const pirk_model* m, int32_t method,
                              const pirk_window* win, const double* p0, const double* p1,
                              double t, double hk, uint64_t step_index, uint64_t* fail_ptr) {
-    return step_window_impl(ctx, m, method, win, nullptr, nullptr, p0, p1, t, hk, step_index, fail_ptr);
+    return step_window_impl(ctx, m, method, win, nullptr, p0, p1, t, hk, step_index, fail_ptr);
 }
 
 pirk_status pirk_step_window_mirror(pirk_ctx* ctx, const pirk_model* m, int32_t method,
-                                    const pirk_window* win, double* mir0, double* mir1,
+                                    const pirk_window* win, const pirk_mirror* mirror,
                                     const double* p0, const double* p1, double t, double hk,
                                     uint64_t step_index, uint64_t* fail_ptr) {
-    if (!mir0 || !mir1) return ctx ? fail(ctx, PIRK_EINVAL, "step_window_mirror: mirror pointers missing")
-                                   : PIRK_EINVAL;
-    return step_window_impl(ctx, m, method, win, mir0, mir1, p0, p1, t, hk, step_index, fail_ptr);
+    if (!mirror) return ctx ? fail(ctx, PIRK_EINVAL, "step_window_mirror: mirror missing") : PIRK_EINVAL;
+    return step_window_impl(ctx, m, method, win, mirror, p0, p1, t, hk, step_index, fail_ptr);
 }
 
 pirk_status pirk_ipc_export(const void* dptr, unsigned char handle[64], uint64_t* offset) {

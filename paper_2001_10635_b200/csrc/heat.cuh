@@ -268,7 +268,9 @@ struct HeatRun {
     const void* tmap;
     int bx0, by0, wbz;
     unsigned long long* bars;
-    double* mdst;  // Mirror: the neighbour lane's halo planes (WindowArgs::mir0/1), indexed like dst
+    double* mdst;  // Mirror: the low neighbour's halo planes (WindowArgs::mir0/1), indexed like dst
+    double* mhdst;  // Mirror: the high neighbour's (WindowArgs::mirh0/1)
+    int m_lo_end, m_hi_begin;  // planes < m_lo_end go to mdst, planes >= m_hi_begin to mhdst
 
     // register state: slot (p - zs) & 3 of plane p
     double ox[2][4], ou1[2][4], ou2[2][4], ou3[2][4];
@@ -287,7 +289,8 @@ struct HeatRun {
     // running plane pointers: x-plane j+1 (loads) and output plane j-4 (stores)
     const double* ldp;
     double* stp;
-    double* mtp;  // Mirror: stp in the neighbour's window
+    double* mtp;  // Mirror: stp in the low neighbour's window
+    double* mhp;  // Mirror: stp in the high neighbour's window
 
     // x-plane p -> x-ring slot s.  TMA: one thread issues the whole 40x40 box
     // (out-of-grid cells zero-filled), completion on bars[s].  Fallback: each
@@ -498,7 +501,10 @@ struct HeatRun {
                                   : fma(hp.h6kk, acc[k] + kk[k], xs[k]);
                     if (in(k)) {
                         out[c.og + k] = xn[k];
-                        if constexpr (Mirror) mtp[c.og + k] = xn[k];
+                        if constexpr (Mirror) {
+                            if (p < m_lo_end) mtp[c.og + k] = xn[k];
+                            if (p >= m_hi_begin) mhp[c.og + k] = xn[k];
+                        }
                     }
                 }
                 // one test per pair: the sum is non-finite whenever either value
@@ -528,7 +534,10 @@ struct HeatRun {
         }
         ldp += g2;
         stp += g2;
-        if constexpr (Mirror) mtp += g2;
+        if constexpr (Mirror) {
+            mtp += g2;
+            mhp += g2;
+        }
         if constexpr (!Tma) cp_async_wait_all();  // x(j+1) landed (own copies); barrier publishes it
         __syncthreads();
     }
@@ -555,7 +564,10 @@ struct HeatRun {
         __syncthreads();
         ldp = src + static_cast<long long>(zs + 1) * g2;
         stp = dst + static_cast<long long>(zs - 4) * g2;
-        if constexpr (Mirror) mtp = mdst + static_cast<long long>(zs - 4) * g2;
+        if constexpr (Mirror) {
+            mtp = mdst + static_cast<long long>(zs - 4) * g2;
+            mhp = mhdst + static_cast<long long>(zs - 4) * g2;
+        }
         const int jend = ze + kHeatH;
         // Steady-state iterations: all four stages valid and planes j-5 .. j
         // clear of the insulated z faces, so the unrolled main loop carries no
@@ -685,12 +697,14 @@ heat_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w,
     const int bx0 = static_cast<int>(ix0) - kHeatH, by0 = static_cast<int>(iy0) - kHeatH;
     const int wbz = static_cast<int>(w.win_begin);
     double* mdst = Mirror ? (field ? w.mir1 : w.mir0) - static_cast<long long>(w.out_begin) * g2 : nullptr;
+    double* mhdst = Mirror ? (field ? w.mirh1 : w.mirh0) - static_cast<long long>(w.out_begin) * g2 : nullptr;
+    const MirrorLimits mlim = MirrorLimits::of(w);
 #define PIRK_HEAT_RUN(INTERIOR, TMA)                                                               \
     {                                                                                              \
         HeatRun<Exact, INTERIOR, TMA, Mirror> r{hp, sc, c, smem, zs, ze, static_cast<int>(obz),   \
                                         static_cast<int>(oez), static_cast<int>(g), zs > 0, ze < g, \
                                         g2, src, dst, field, m.method, step, fail, n_total, tmap,  \
-                                        bx0, by0, wbz, bars, mdst};                                \
+                                        bx0, by0, wbz, bars, mdst, mhdst, mlim.lo_end, mlim.hi_begin};                                \
         r.tacc = tacc;                                                                             \
         r.run();                                                                                   \
     }

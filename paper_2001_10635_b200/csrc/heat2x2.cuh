@@ -105,7 +105,9 @@ struct Heat2Run {
     const void* tmap;
     int bx0, by0, wbz;
     unsigned long long* bars;
-    double* mdst;  // Mirror: the neighbour lane's halo planes, indexed like dst
+    double* mdst;  // Mirror: the low neighbour's halo planes, indexed like dst
+    double* mhdst;  // Mirror: the high neighbour's
+    int m_lo_end, m_hi_begin;  // planes < m_lo_end go to mdst, planes >= m_hi_begin to mhdst
 
     // own block: [point k][plane slot (p - zs) & 3]
     double ox[4][4], ou1[4][4], ou2[4][4], ou3[4][4];
@@ -116,7 +118,8 @@ struct Heat2Run {
     bool vec;  // outputs 16-byte aligned at even offsets (g even, aligned windows)
     const double* ldp;
     double* stp;
-    double* mtp;  // Mirror: stp in the neighbour's window
+    double* mtp;  // Mirror: stp in the low neighbour's window
+    double* mhp;  // Mirror: stp in the high neighbour's window
 
     __device__ __forceinline__ bool in(int k) const { return Interior || (c.of[k] & kIn); }
     __device__ __forceinline__ int goff(int k) const { return c.og + (k & 1) + (k >> 1) * g; }
@@ -381,9 +384,16 @@ struct Heat2Run {
                         if (in(k)) out[(k & 1) + (k >> 1) * g] = xn[k];
                 }
                 if constexpr (Mirror) {
+                    if (p < m_lo_end) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (in(k)) mtp[c.og + (k & 1) + (k >> 1) * g] = xn[k];
+                        for (int k = 0; k < 4; ++k)
+                            if (in(k)) mtp[c.og + (k & 1) + (k >> 1) * g] = xn[k];
+                    }
+                    if (p >= m_hi_begin) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (in(k)) mhp[c.og + (k & 1) + (k >> 1) * g] = xn[k];
+                    }
                 }
                 if (!finite_d((xn[0] + xn[1]) + (xn[2] + xn[3]))) {
 #pragma unroll
@@ -413,7 +423,10 @@ struct Heat2Run {
         }
         ldp += g2;
         stp += g2;
-        if constexpr (Mirror) mtp += g2;
+        if constexpr (Mirror) {
+            mtp += g2;
+            mhp += g2;
+        }
         if constexpr (!Tma) cp_async_wait_all();
         __syncthreads();
     }
@@ -440,7 +453,10 @@ struct Heat2Run {
         __syncthreads();
         ldp = src + static_cast<long long>(zs + 1) * g2;
         stp = dst + static_cast<long long>(zs - 4) * g2;
-        if constexpr (Mirror) mtp = mdst + static_cast<long long>(zs - 4) * g2;
+        if constexpr (Mirror) {
+            mtp = mdst + static_cast<long long>(zs - 4) * g2;
+            mhp = mhdst + static_cast<long long>(zs - 4) * g2;
+        }
         const int jend = ze + kHeatH;
         // steady-state bounds: as HeatRun::run
         int a = zs + 3 + 3 * lo_shift;
@@ -559,12 +575,14 @@ heat2_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
     const int bx0 = static_cast<int>(ix0) - kHeatH, by0 = static_cast<int>(iy0) - kHeatH;
     const int wbz = static_cast<int>(w.win_begin);
     double* mdst = Mirror ? (field ? w.mir1 : w.mir0) - static_cast<long long>(w.out_begin) * g2 : nullptr;
+    double* mhdst = Mirror ? (field ? w.mirh1 : w.mirh0) - static_cast<long long>(w.out_begin) * g2 : nullptr;
+    const MirrorLimits mlim = MirrorLimits::of(w);
 #define PIRK_HEAT2_RUN(INTERIOR, TMA)                                                              \
     {                                                                                              \
         Heat2Run<Exact, INTERIOR, TMA, Mirror> r{hp, sc, c, smem, zs, ze, static_cast<int>(obz),  \
                                          static_cast<int>(oez), static_cast<int>(g), zs > 0,      \
                                          ze < g, g2, src, dst, field, m.method, step, fail,        \
-                                         n_total, tmap, bx0, by0, wbz, bars, mdst};                \
+                                         n_total, tmap, bx0, by0, wbz, bars, mdst, mhdst, mlim.lo_end, mlim.hi_begin};                \
         r.tacc = tacc;                                                                             \
         r.vec = (flags & 2) != 0;                                                                  \
         r.run();                                                                                   \
@@ -698,7 +716,7 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
             if (field_only >= 0)
                 heat_strip_kernel<Exact, true><<<grid, kSThreads, kSSmemBytes, stream>>>(
                     m, hp, w, sc, step, zchunk, fail, tm, 1 | (vec ? 2 : 0) | fsel);
-            else if (w.mir0)
+            else if (w.mirrored())
                 heat_strip_kernel<Exact, false, true><<<grid, kSThreads, kSSmemBytes, stream>>>(
                     m, hp, w, sc, step, zchunk, fail, tm, 1 | (vec ? 2 : 0));
             else
@@ -732,13 +750,13 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
     const int tma = heat_encode_tmap(&tm.f[0], w.in0, m.g, wplanes) &&
                     heat_encode_tmap(&tm.f[1], w.in1, m.g, wplanes);
     if (variant >= 1) {
-        if (w.mir0)
+        if (w.mirrored())
             heat2_step_kernel<Exact, true><<<grid, kHeat2Threads, kHeatSmemBytes, stream>>>(
                 m, hp, w, sc, step, zchunk, fail, tm, tma | (vec ? 2 : 0));
         else
             heat2_step_kernel<Exact><<<grid, kHeat2Threads, kHeatSmemBytes, stream>>>(
                 m, hp, w, sc, step, zchunk, fail, tm, tma | (vec ? 2 : 0));
-    } else if (w.mir0) {
+    } else if (w.mirrored()) {
         heat_step_kernel<Exact, true><<<grid, kHeatThreads, kHeatSmemBytes, stream>>>(m, hp, w, sc, step, zchunk,
                                                                                       fail, tm, tma);
     } else {

@@ -144,7 +144,9 @@ struct HeatStrip {
     int zs, ze, ob, oe, g, lo_shift, hi_shift;
     long long g2;
     double* __restrict__ stp;  // output plane j-4 at the own block's (0,0)
-    double* mtp;               // Mirror: stp in the neighbour lane's window
+    double* mtp;               // Mirror: stp in the low neighbour's window (planes < m_lo_end)
+    double* mhp;               // Mirror: stp in the high neighbour's window (planes >= m_hi_begin)
+    int m_lo_end, m_hi_begin;
     bool st_own;               // own block with all 8 cells in the grid (vector stores)
     unsigned st_mask;          // edge tiles: per-cell store mask (bit 2r+c)
     int gout;                  // in-plane global offset of the block's (0,0) cell
@@ -506,11 +508,18 @@ struct HeatStrip {
                     for (int i = 0; i < 8; ++i)
                         if ((st_mask >> i) & 1) stp[(i >> 1) * g + (i & 1)] = y[i];
                 }
-                if constexpr (Mirror) {  // the same cells into the neighbour's halo, over peer memory
+                if constexpr (Mirror) {  // the same cells into the neighbours' halos, over peer memory
                     const unsigned mk = st_own ? 0xffu : st_mask;
+                    if (j - 4 < m_lo_end) {
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
-                        if ((mk >> i) & 1) mtp[(i >> 1) * g + (i & 1)] = y[i];
+                        for (int i = 0; i < 8; ++i)
+                            if ((mk >> i) & 1) mtp[(i >> 1) * g + (i & 1)] = y[i];
+                    }
+                    if (j - 4 >= m_hi_begin) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+                            if ((mk >> i) & 1) mhp[(i >> 1) * g + (i & 1)] = y[i];
+                    }
                 }
                 if ((st_own || st_mask) &&
                     !finite_d(((y[0] + y[1]) + (y[2] + y[3])) + ((y[4] + y[5]) + (y[6] + y[7]))))
@@ -534,7 +543,10 @@ struct HeatStrip {
             xs = (xs + 1) & 3;
         }
         stp += g2;
-        if constexpr (Mirror) mtp += g2;
+        if constexpr (Mirror) {
+            mtp += g2;
+            mhp += g2;
+        }
         // one barrier per plane: this iteration's rows (buffer j & 1) become
         // readable, and the next iteration may overwrite buffer (j - 1) & 1
         if constexpr (PIRK_STRIP_SPLITBAR) {
@@ -635,6 +647,8 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
     const int ze = static_cast<int>((oez + kHeatH < g) ? oez + kHeatH : g);
     double* dst = (field ? w.out1 : w.out0) - static_cast<long long>(w.out_begin) * g2;
     double* mdst = Mirror ? (field ? w.mir1 : w.mir0) - static_cast<long long>(w.out_begin) * g2 : nullptr;
+    double* mhdst = Mirror ? (field ? w.mirh1 : w.mirh0) - static_cast<long long>(w.out_begin) * g2 : nullptr;
+    const MirrorLimits mlim = MirrorLimits::of(w);
 
     if (warp == 0) tmem_alloc512(&tmem_base);
     if (tid == 0) {
@@ -663,7 +677,11 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
         r.g2 = g2;                                                                                   \
         r.gout = gout;                                                                               \
         r.stp = dst + static_cast<long long>(zs - 4) * g2 + gout;                                    \
-        if constexpr (Mirror) r.mtp = mdst + static_cast<long long>(zs - 4) * g2 + gout;             \
+        if constexpr (Mirror) {                                                                      \
+            r.mtp = mdst + static_cast<long long>(zs - 4) * g2 + gout;                               \
+            r.mhp = mhdst + static_cast<long long>(zs - 4) * g2 + gout;                              \
+            r.m_lo_end = mlim.lo_end, r.m_hi_begin = mlim.hi_begin;                                  \
+        }                                                                                            \
         r.st_own = st_own, r.st_mask = st_mask;                                                      \
         r.fx0 = fx0, r.fxg = fxg, r.fy0 = fy0, r.fyg = fyg;                                          \
         r.field = field, r.method = m.method, r.step = step, r.fail = fail;                          \

@@ -18,11 +18,33 @@ struct WindowArgs {
     double* out1;
     uint64_t win_begin, win_end;
     uint64_t out_begin, out_end;
-    // mirror outputs (or null): every value stored to out0[k] / out1[k] is also
-    // stored to mir0[k] / mir1[k] -- a neighbour lane's halo over NVLink peer
-    // memory, written by the kernel that computes it (engine.cu run_large_multi)
+    // mirror outputs (or null): a value of unit u stored to out0[k] / out1[k]
+    // (k = u - out_begin) is also stored to mir0[k] / mir1[k] when
+    // u < mir_lo_end, and to mirh0[k] / mirh1[k] when u >= mir_hi_begin -- the
+    // neighbours' halos over NVLink peer memory, written by the kernel that
+    // computes them (engine.cu run_large_multi, sharded.PeerStores).  The
+    // defaults mirror every unit to mir0/1 and none to mirh0/1.
     double* mir0 = nullptr;
     double* mir1 = nullptr;
+    uint64_t mir_lo_end = ~0ull;
+    double* mirh0 = nullptr;
+    double* mirh1 = nullptr;
+    uint64_t mir_hi_begin = ~0ull;
+
+    __host__ __device__ bool mirrored() const { return mir0 != nullptr || mirh0 != nullptr; }
+};
+
+// Per-launch plane limits of the two mirror targets as ints (planes < 2^31):
+// units u < lo_end go to the low target, u >= hi_begin to the high one.
+struct MirrorLimits {
+    int lo_end, hi_begin;
+    __host__ __device__ static MirrorLimits of(const WindowArgs& w) {
+        MirrorLimits m;
+        m.lo_end = !w.mir0 ? -0x7fffffff : (w.mir_lo_end >= 0x7fffffffull ? 0x7fffffff : static_cast<int>(w.mir_lo_end));
+        m.hi_begin = !w.mirh0 ? 0x7fffffff : (w.mir_hi_begin >= 0x7fffffffull ? 0x7fffffff
+                                                                                : static_cast<int>(w.mir_hi_begin));
+        return m;
+    }
 };
 
 // 1-D radius-1 models on two fields (traffic MM/GB, coupled chain MM).

@@ -606,8 +606,10 @@ def step_window(model: SystemModel, method: str, in0_ptr: int, in1_ptr: int, out
                 step_index: int, fail_ptr: int = 0, *, ctx: Optional[Context] = None,
                 mirror=None) -> None:
     """pirk_step_window on caller-owned device buffers (raw pointers).  With
-    ``mirror=(m0, m1)`` (pirk_step_window_mirror) every output unit is also
-    stored to m0 / m1, indexed like out0 / out1 (a peer's window)."""
+    ``mirror=(lo0, lo1, lo_end, hi0, hi1, hi_begin)`` (pirk_step_window_mirror)
+    output units u < lo_end are also stored to lo0/lo1 and units u >= hi_begin
+    to hi0/hi1, indexed like out0/out1 (the neighbours' windows; a None
+    pointer pair disables that side)."""
     ctx = ctx or get_context()
     m = model_struct(model)
     w = _lib.PirkWindow(in0_ptr, in1_ptr, out0_ptr, out1_ptr, win_begin, win_len, out_begin,
@@ -620,6 +622,8 @@ def step_window(model: SystemModel, method: str, in0_ptr: int, in1_ptr: int, out
                                               _lib.dptr(a0), _lib.dptr(a1), float(t), float(hk),
                                               int(step_index), C.c_void_p(fail_ptr)))
     else:
+        lo0, lo1, lo_end, hi0, hi1, hi_begin = mirror
+        mr = _lib.PirkMirror(lo0, lo1, int(lo_end) if lo0 else 0, hi0, hi1, int(hi_begin) if hi0 else 0)
         ctx.check(_lib.lib().pirk_step_window_mirror(
-            ctx.handle, C.byref(m), code, C.byref(w), C.c_void_p(mirror[0]), C.c_void_p(mirror[1]),
+            ctx.handle, C.byref(m), code, C.byref(w), C.byref(mr),
             _lib.dptr(a0), _lib.dptr(a1), float(t), float(hk), int(step_index), C.c_void_p(fail_ptr)))

@@ -162,12 +162,22 @@ class PeerStores:
     the buffer its step k-1 read, and its flag k-1 is raised only after its
     boundary launch (the only reader of the halo) of step k-1.
 
+    ``fused=True`` (default) runs each step as ONE launch over the rank's
+    slab that stores its first and last 4 units into the neighbours' windows
+    as it computes them:
+        wait(neighbour flags >= k-1) | whole slab (+ peer stores) | signal(k)
+    A windowed launch pays a fixed cost (the 8-plane z cone and CTA set-up
+    over all tiles, ~0.5 ms for heat3d g=1600) however thin it is, so two
+    4-unit boundary launches per step cost more than the overlap they buy
+    when ranks run in lockstep.  ``fused=False`` keeps the boundary-first
+    schedule above.
+
     Only the control plane (handle exchange, barriers) uses
     torch.distributed, so it runs over NCCL or gloo alike -- on one GPU
     several processes test the same path with device-local "peer" stores.
     Requires K = 1 (halo 4) and every shard at least 8 units wide."""
 
-    def __init__(self, shard: Shard, unit: int, ctx, group=None):
+    def __init__(self, shard: Shard, unit: int, ctx, group=None, fused: bool = True):
         import torch.distributed as dist
 
         self.dist = dist
@@ -175,6 +185,7 @@ class PeerStores:
         self.unit = unit
         self.ctx = ctx
         self.group = group
+        self.fused = fused
         self.seq = 0
         self._bases = []
         if shard.world > 1 and shard.end - shard.begin < 8:
@@ -270,14 +281,25 @@ class PeerStores:
             if side in self.nb:
                 self._on_stream(_lib.lib().pirk_signal_flag, self.nb[side]["flags"] + 4 * slot, value)
 
-    def mirror(self, side: str, out0, out_begin: int):
-        """(m0, m1): the neighbour's output buffers at unit out_begin -- the
-        buffer with the same role (A or B) as this rank's out0, since all ranks
-        swap in lockstep."""
-        idx = [t.data_ptr() for t in self.local].index(out0.data_ptr())
+    def _target(self, side: str, idx: int, out_begin: int):
+        """Device address of unit out_begin in the neighbour's buffer idx (the
+        address may lie outside that window; only its halo units are stored)."""
         nb = self.nb[side]
-        off = (out_begin - nb["win_begin"]) * self.unit * 8
-        return nb["bufs"][idx] + off, nb["bufs"][idx + 1] + off
+        return nb["bufs"][idx] + (out_begin - nb["win_begin"]) * self.unit * 8
+
+    def mirror(self, out0, out_begin: int, out_end: int):
+        """pirk_step_window_mirror arguments for a launch over [out_begin,
+        out_end): its first 4 units to the left neighbour, its last 4 to the
+        right one, into the buffers with the same role (A or B) as this rank's
+        out0 -- all ranks swap in lockstep."""
+        idx = [t.data_ptr() for t in self.local].index(out0.data_ptr())
+        lo = hi = (None, None)
+        s = self.shard
+        if "left" in self.nb and out_begin < s.begin + 4:
+            lo = (self._target("left", idx, out_begin), self._target("left", idx + 1, out_begin))
+        if "right" in self.nb and out_end > s.end - 4:
+            hi = (self._target("right", idx, out_begin), self._target("right", idx + 1, out_begin))
+        return lo[0], lo[1], s.begin + 4, hi[0], hi[1], s.end - 4
 
 
 def device_step_fn(model: SystemModel, method: str, ctx=None):
@@ -430,13 +452,19 @@ class ShardedReach:
             ex.seq += 1
             ex.wait(ex.seq - 1)
             a, b = self.a, self.b
-            for side, (blo, bhi) in (("left", (s.begin, s.begin + 4)), ("right", (s.end - 4, s.end))):
-                if side in ex.nb:
-                    self.step_fn(a[0], a[1], b[0], b[1], *args, blo, bhi, self.p0, self.p1, t, hk, k0 + i,
-                                 fp, mirror=ex.mirror(side, b[0], blo))
-            ex.signal(ex.seq)
-            if ilo < ihi:
-                self.step_fn(a[0], a[1], b[0], b[1], *args, ilo, ihi, self.p0, self.p1, t, hk, k0 + i, fp)
+            if ex.fused:
+                mir = ex.mirror(b[0], s.begin, s.end) if ex.nb else None
+                self.step_fn(a[0], a[1], b[0], b[1], *args, s.begin, s.end, self.p0, self.p1, t, hk, k0 + i,
+                             fp, mirror=mir)
+                ex.signal(ex.seq)
+            else:
+                for side, (blo, bhi) in (("left", (s.begin, s.begin + 4)), ("right", (s.end - 4, s.end))):
+                    if side in ex.nb:
+                        self.step_fn(a[0], a[1], b[0], b[1], *args, blo, bhi, self.p0, self.p1, t, hk, k0 + i,
+                                     fp, mirror=ex.mirror(b[0], blo, bhi))
+                ex.signal(ex.seq)
+                if ilo < ihi:
+                    self.step_fn(a[0], a[1], b[0], b[1], *args, ilo, ihi, self.p0, self.p1, t, hk, k0 + i, fp)
             self.a, self.b = b, a
 
     def owned(self):

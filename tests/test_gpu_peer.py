@@ -44,7 +44,7 @@ def _problem(kind):
     return m, "mixed-monotonicity", lo, lo + 0.2, None, None, 0.0, 0.002, 0.0003
 
 
-def _worker(rank, world, port, kind, mode, q):
+def _worker(rank, world, port, kind, mode, q, fused=True):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch
@@ -60,7 +60,7 @@ def _worker(rank, world, port, kind, mode, q):
         units, unit = S.units_of(m)
         ctx = pk.Context(0, mode)
         shard = S.Shard(units, world, rank, 4)
-        ex = S.PeerStores(shard, unit, ctx)
+        ex = S.PeerStores(shard, unit, ctx, fused=fused)
         run = S.ShardedReach(m, method, shard, S.device_step_fn(m, method, ctx), ex, p0, p1, K=1)
         dev = torch.device("cuda", 0)
         fail = torch.full((2,), -1, dtype=torch.int64, device=dev)
@@ -87,17 +87,18 @@ def _worker(rank, world, port, kind, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,world,mode", [("heat", 2, "exact"), ("heat", 3, "fast"),
-                                             ("traffic", 3, "exact"), ("chain", 4, "exact"),
-                                             ("traffic_gb", 2, "exact"),
-                                             ("heat", 2, "fast")])
-def test_peer_store_processes_equal_single(kind, world, mode):
+@pytest.mark.parametrize("kind,world,mode,fused", [("heat", 2, "exact", True), ("heat", 3, "fast", True),
+                                                   ("traffic", 3, "exact", True), ("chain", 4, "exact", True),
+                                                   ("traffic_gb", 2, "exact", True), ("heat", 2, "fast", True),
+                                                   ("heat", 3, "fast", False), ("heat", 3, "exact", False),
+                                                   ("chain", 3, "exact", False)])
+def test_peer_store_processes_equal_single(kind, world, mode, fused):
     import torch.multiprocessing as mp
 
     ctxm = mp.get_context("spawn")
     q = ctxm.Queue()
     port = _free_port()
-    procs = [ctxm.Process(target=_worker, args=(r, world, port, kind, mode, q)) for r in range(world)]
+    procs = [ctxm.Process(target=_worker, args=(r, world, port, kind, mode, q, fused)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}

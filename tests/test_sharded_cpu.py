@@ -214,20 +214,20 @@ class _LockstepPeers(S.PeerStores):
     def signal(self, value):
         self.signals.append(value)
 
-    def mirror(self, side, out0, out_begin):
-        idx = [t.data_ptr() for t in self.local].index(out0.data_ptr())
+    def _target(self, side, idx, out_begin):
         nb = self.nb[side]
-        off = (out_begin - nb["win_begin"]) * self.unit
-        return nb["bufs"][idx][off:], nb["bufs"][idx + 1][off:]
+        return nb["bufs"][idx], out_begin - nb["win_begin"]
 
 
-@pytest.mark.parametrize("kind,world", [("traffic", 2), ("traffic", 3), ("chain", 4), ("heat", 2),
-                                        ("heat", 3), ("traffic_gb", 2)])
-def test_peer_store_schedule_equals_single(kind, world):
-    """The peer-store schedule (boundary units first, stored into the
-    neighbours' windows, then the interior) with the oracle's windowed step,
-    which reads NaN outside its window: bit-identical to one process, and the
-    flag protocol waits for k-1 before raising k on every step."""
+@pytest.mark.parametrize("kind,world,fused", [("traffic", 2, True), ("traffic", 3, True), ("chain", 4, True),
+                                              ("heat", 2, True), ("heat", 3, True), ("traffic_gb", 2, True),
+                                              ("traffic", 3, False), ("heat", 3, False), ("chain", 4, False)])
+def test_peer_store_schedule_equals_single(kind, world, fused):
+    """The peer-store schedules (fused: one launch per slab storing its edge
+    units into the neighbours' windows; split: boundary units first, then the
+    interior) with the oracle's windowed step, which reads NaN outside its
+    window: bit-identical to one process, and the flag protocol waits for k-1
+    before raising k on every step."""
     m, method, lo, hi, plo, phi, t0, t1, h = problem(kind)
     units, unit = S.units_of(m)
     if method == "growth-bound":
@@ -239,15 +239,26 @@ def test_peer_store_schedule_equals_single(kind, world):
 
     def step(in0, in1, out0, out1, wb, wl, lo_, hi_, p0_, p1_, t, hk, k, fail_ptr=0, mirror=None):
         base(in0, in1, out0, out1, wb, wl, lo_, hi_, p0_, p1_, t, hk, k)
-        if mirror is not None:
-            a, n = (lo_ - wb) * unit, (hi_ - lo_) * unit
-            mirror[0][:n] = out0[a:a + n]
-            mirror[1][:n] = out1[a:a + n]
+        if mirror is None:
+            return
+        lo0, lo1, lo_end, hi0, hi1, hi_begin = mirror
+
+        def put(t0, t1, u0, u1):  # units [u0, u1) into the target pair
+            if t0 is None or u0 >= u1:
+                return
+            (d0, off), (d1, _) = t0, t1
+            a, n, b = (u0 - wb) * unit, (u1 - u0) * unit, (u0 - lo_ + off) * unit
+            assert b >= 0
+            d0[b:b + n] = out0[a:a + n]
+            d1[b:b + n] = out1[a:a + n]
+        put(lo0, lo1, lo_, min(hi_, lo_end))
+        put(hi0, hi1, max(lo_, hi_begin), hi_)
 
     runs, exs = [], []
     for r in range(world):
         shard = S.Shard(units, world, r, 4)
         ex = _LockstepPeers(shard, unit)
+        ex.fused = fused
         run = S.ShardedReach(m, method, shard, step, ex, p0, p1, K=1)
         a = run.alloc(lambda n: torch.full((n,), float("nan"), dtype=torch.float64))
         sl = slice(shard.win_begin * unit, shard.win_end * unit)
