@@ -1093,15 +1093,21 @@ pirk_status run_large(pirk_ctx* ctx, const pirk_model* m, int method, const pirk
 // z-slabs (models.cpp:110-112), exactly as sharded.py does across processes.
 // Each lane keeps a window of its units plus a 4-unit halo per side (the RK4
 // dependency cone of a radius-1 stencil) and exchanges halos every step.  By
-// default the boundary launch itself stores its units into the neighbours'
-// halos over NVLink peer memory (WindowArgs::mir0/1); PIRK_LANE_HALO=copy, or
-// lanes without peer access, use copy-engine peer copies instead:
+// default ONE launch per lane and step computes its owned units and stores the
+// first / last 4 of them a second time into the neighbours' halos over NVLink
+// peer memory (WindowArgs::mir0/1, mirh0/1):
+//
+//   lane stream:  wait(neighbours' step k-1) | owned units (+ edge units to the neighbours)
+//
+// PIRK_LANE_SCHEDULE=split runs the boundary units as separate launches first
+// (their stores overlap the interior launch); PIRK_LANE_HALO=copy, or lanes
+// without peer access, send them with copy-engine peer copies instead:
 //
 //   lane stream:  wait(halos of step k-1) | boundary units (+ peer stores) | interior ....
 //   lane copies:                          | (copy mode) send boundary -> neighbours' halos
 //
-// The boundary units (the ones the neighbours need next step) are computed
-// first, their transfer overlaps the interior, and the next
+// In the split schedules the boundary units (the ones the neighbours need next
+// step) are computed first, their transfer overlaps the interior, and the next
 // step waits only for the copies (double-buffered events: a lane waits on
 // its neighbours' step-(k-1) records, never on the current ones).  Every unit
 // is computed once from the same inputs as on one device, so the result is
@@ -1224,15 +1230,37 @@ pirk_status run_large_multi(pirk_ctx* ctx, const pirk_model* m, int method, cons
         return v && std::strcmp(v, "copy") == 0;
     }();
     const bool fused = ctx->peer_stores && !halo_copy_env;
+    // Fused halos, by default as ONE launch per lane and step over its owned
+    // units whose first / last 4 units also go to the neighbours (a windowed
+    // launch has a fixed cost -- the 4-unit cone on both sides and the CTA
+    // set-up over every tile -- so two thin boundary launches per step cost
+    // more than the overlap they buy: tools/peer_probe.py, heat3d g=1600 over
+    // 8 lanes 4.94 vs 5.69 ms per step).  PIRK_LANE_SCHEDULE=split keeps the
+    // boundary-first launches.
+    static const bool split_env = [] {
+        const char* v = std::getenv("PIRK_LANE_SCHEDULE");
+        return v && std::strcmp(v, "split") == 0;
+    }();
+    const bool slab = fused && !split_env;
     auto launch = [&](ShardState& z, const StepConsts& sc, uint64_t k, uint64_t ob, uint64_t oe,
-                      ShardState* mirror = nullptr) -> cudaError_t {
+                      ShardState* mlo = nullptr, ShardState* mhi = nullptr) -> cudaError_t {
         if (ob >= oe) return cudaSuccess;
         const size_t off = (ob - z.wb) * unit;
         WindowArgs w{z.in0(), z.in1(), z.out0() + off, z.out1() + off, z.wb, z.we, ob, oe};
-        if (mirror) {  // unit ob at the same place of the neighbour's output window
-            const size_t moff = (ob - mirror->wb) * unit;
-            w.mir0 = mirror->out0() + moff;
-            w.mir1 = mirror->out1() + moff;
+        // mirror targets: unit ob at the same place of the neighbour's output
+        // window (for the high neighbour that place lies before its window;
+        // only units >= its window start are stored)
+        if (mlo) {
+            const long long moff = (static_cast<long long>(ob) - static_cast<long long>(mlo->wb)) * unit;
+            w.mir0 = mlo->out0() + moff;
+            w.mir1 = mlo->out1() + moff;
+            w.mir_lo_end = z.b + 4;
+        }
+        if (mhi) {
+            const long long moff = (static_cast<long long>(ob) - static_cast<long long>(mhi->wb)) * unit;
+            w.mirh0 = mhi->out0() + moff;
+            w.mirh1 = mhi->out1() + moff;
+            w.mir_hi_begin = z.e - 4;
         }
         ctx->launches++;
         if (is_chain(m))
@@ -1261,8 +1289,13 @@ pirk_status run_large_multi(pirk_ctx* ctx, const pirk_model* m, int method, cons
                 //    (fused: written into the neighbours' halos by the same launch)
                 ShardState* yl = left ? &sh[static_cast<size_t>(r - 1)] : nullptr;
                 ShardState* yr = right ? &sh[static_cast<size_t>(r + 1)] : nullptr;
+                if (slab) {  // one launch: owned units, edges also into the neighbours' halos
+                    CK(ctx, launch(z, sc, k, z.b, z.e, yl, yr));
+                    if (left || right) CK(ctx, cudaEventRecord(z.sent[k & 1], z.L.s));
+                    continue;
+                }
                 if (left) CK(ctx, launch(z, sc, k, z.b, z.b + 4, fused ? yl : nullptr));
-                if (right) CK(ctx, launch(z, sc, k, z.e - 4, z.e, fused ? yr : nullptr));
+                if (right) CK(ctx, launch(z, sc, k, z.e - 4, z.e, nullptr, fused ? yr : nullptr));
                 if (fused && (left || right)) CK(ctx, cudaEventRecord(z.sent[k & 1], z.L.s));
                 // 2. else their peer copies, on the copy stream
                 if (!fused && (left || right)) {

@@ -234,6 +234,21 @@ def test_copy_engine_halo_path():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, PIRK_LANE_HALO="copy")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
-                        os.path.join(root, "tests", "test_gpu_multilane.py"), "-k", "lanes and not copy"],
+                        os.path.join(root, "tests", "test_gpu_multilane.py"), "-k", "lanes and not copy and not split"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_split_lane_schedule():
+    """PIRK_LANE_SCHEDULE=split: boundary units as separate launches first
+    (their peer stores overlap the interior launch) instead of the default one
+    launch per lane and step -- same bit-identical results."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PIRK_LANE_SCHEDULE="split")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        os.path.join(root, "tests", "test_gpu_multilane.py"), "-k", "lanes and not copy and not split"],
                        env=env, cwd=root, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
