@@ -146,6 +146,21 @@ def halo_exchanger(args, S, shard, unit, ctx, world):
     return S.HaloExchanger(shard, unit)
 
 
+def attach_or_nccl(args, S, run, ex, shard, unit):
+    """Map the neighbours' windows for peer stores; if some neighbouring GPUs
+    cannot address each other (every rank learns it together), the run uses
+    NCCL halo exchange instead and the line says so (args.halo)."""
+    if not isinstance(ex, S.PeerStores):
+        return ex
+    try:
+        ex.attach(run)
+        return ex
+    except S.PeerUnavailable:
+        args.halo = "nccl"
+        run.ex = S.HaloExchanger(shard, unit)
+        return run.ex
+
+
 HALO_DESC = {"peer": "halos stored into the neighbours' windows by the boundary launches (CUDA IPC peer memory)",
              "nccl": "NCCL halo exchange"}
 
@@ -175,8 +190,7 @@ def heat_device_bench(args, world, rank, local, torch, pk, dist):
     dev = torch.device("cuda", local)
     fail = torch.full((2,), -1, dtype=torch.int64, device=dev)  # device failure keys
     a = run.alloc(lambda n: torch.empty(n, dtype=torch.float64, device=dev), fail=fail)
-    if isinstance(ex, S.PeerStores):
-        ex.attach(run)
+    ex = attach_or_nccl(args, S, run, ex, shard, unit)
     a[0].fill_(0.9)  # catalog default box [0.9, 1.1] (models.cpp:744-745)
     a[1].fill_(1.1)
     steps = [(float(k) * args.h, args.h) for k in range(args.warmup + args.steps)]
@@ -348,8 +362,7 @@ def heat_e2e_sharded(args, pk, torch, dist, world, rank, local):
     steps = S.plan_rk4_steps(0.0, C5_STEPS * args.h, args.h)
     fail = torch.full((2,), -1, dtype=torch.int64, device=dev)
     a = run.alloc(lambda k: torch.empty(k, dtype=torch.float64, device=dev), fail=fail)
-    if isinstance(ex, S.PeerStores):
-        ex.attach(run)
+    ex = attach_or_nccl(args, S, run, ex, shard, unit)
     stream = torch.cuda.Stream(device=dev)
 
     def once():

@@ -147,6 +147,11 @@ class HaloExchanger:
             dev.copy_(host)
 
 
+class PeerUnavailable(RuntimeError):
+    """Neighbouring ranks' GPUs cannot map each other's memory (raised on
+    every rank alike by PeerStores.attach)."""
+
+
 class PeerStores:
     """Halo exchange without a separate transfer, one process per GPU: the
     launch that computes a rank's 4 boundary units stores them a second time,
@@ -219,7 +224,10 @@ class PeerStores:
 
     def attach(self, run: "ShardedReach"):
         """Export this rank's window buffers and flags, map the neighbours'.
-        Collective over the group; call after run.alloc()."""
+        Collective over the group; call after run.alloc().  Raises
+        PeerUnavailable on every rank (before mapping anything) when some pair
+        of neighbouring GPUs cannot address each other's memory -- the caller
+        then uses HaloExchanger."""
         import torch
 
         s = self.shard
@@ -227,10 +235,21 @@ class PeerStores:
         self.flags = torch.zeros(2, dtype=torch.int32, device=dev)  # [from left, from right]
         self.local = [run.a[0], run.a[1], run.b[0], run.b[1]]
         mine = {"win_begin": s.win_begin, "bufs": [self._export(t) for t in self.local],
-                "flags": self._export(self.flags)}
+                "flags": self._export(self.flags), "device": dev.index,
+                "uuid": str(torch.cuda.get_device_properties(dev).uuid)}
         torch.cuda.synchronize(dev)  # flags zeroed before any neighbour can raise them
         allv = [None] * s.world
         self.dist.all_gather_object(allv, mine, group=self.group)
+        # every rank checks its own neighbours, then all agree on the outcome
+        ok = True
+        for r in (s.rank - 1, s.rank + 1):
+            if 0 <= r < s.world and allv[r]["uuid"] != mine["uuid"]:
+                peer = self._local_index(allv[r]["uuid"])
+                ok = ok and peer is not None and torch.cuda.can_device_access_peer(dev.index, peer)
+        oks = [None] * s.world
+        self.dist.all_gather_object(oks, ok, group=self.group)
+        if not all(oks):
+            raise PeerUnavailable("peer-store halos need peer access between neighbouring GPUs")
         self.nb = {}
         for side, r in (("left", s.rank - 1), ("right", s.rank + 1)):
             if 0 <= r < s.world:
@@ -239,6 +258,16 @@ class PeerStores:
                                  "bufs": [self._open(dev.index, *b) for b in o["bufs"]],
                                  "flags": self._open(dev.index, *o["flags"])}
         self.dist.barrier(group=self.group)
+
+    @staticmethod
+    def _local_index(uuid: str):
+        """This process's index of the device with that UUID (None if not visible)."""
+        import torch
+
+        for i in range(torch.cuda.device_count()):
+            if str(torch.cuda.get_device_properties(i).uuid) == uuid:
+                return i
+        return None
 
     def close(self):
         """Unmap the neighbours' buffers once every rank is done with them."""
