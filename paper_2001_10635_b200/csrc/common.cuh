@@ -30,6 +30,20 @@ struct ModeCheck {
 __device__ __forceinline__ double ref_min(double a, double b) { return (b < a) ? b : a; }
 
 // Non-finite check without relying on fast-math-sensitive isfinite.
+// Cheap screen over 8 doubles on the FP32 pipe: the high word of a double
+// read as a float is inf / NaN whenever the double is (its exponent bits 30..23
+// are all ones).  A float sum of the 8 words is therefore non-finite whenever
+// some value is; it can also be non-finite for finite values >= 2^1009 (huge
+// words overflowing the float sum), so a true result only means "check each
+// value with finite_d" (the callers' cold paths do).
+__device__ __forceinline__ bool maybe_nonfinite8(const double (&y)[8]) {
+    float f[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = __int_as_float(__double2hiint(y[i]));
+    const float s = ((f[0] + f[1]) + (f[2] + f[3])) + ((f[4] + f[5]) + (f[6] + f[7]));
+    return (__float_as_int(s) & 0x7f800000) == 0x7f800000;
+}
+
 __device__ __forceinline__ bool finite_d(double v) {
     const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
     return ((b >> 52) & 0x7ffull) != 0x7ffull;

@@ -671,6 +671,15 @@ struct EventGuard {
 
 // The launcher's kernel choice can be overridden (PIRK_HEAT_BLOCK); one-field
 // launches need the strip kernel.
+// every step of the plan can run the fast strip kernel (its S form needs
+// z = hk*kk in range; a tiny remainder step does not qualify)
+bool heat_plan_strip_ok(const pirk_model* m, const pirk_problem* p, const Plan& pl) {
+    const HeatModel hm = heat_model(m, PIRK_METHOD_MM);
+    if (pl.total == 0) return true;
+    if (pl.total > 1 && !heat_strip_step_ok(hm, host_step(p->t0, p->t1, p->h, 0, pl.total).hk)) return false;
+    return heat_strip_step_ok(hm, host_step(p->t0, p->t1, p->h, pl.total - 1, pl.total).hk);
+}
+
 bool heat_single_field_ok() {
     const char* v = std::getenv("PIRK_HEAT_BLOCK");
     return !v || std::strcmp(v, "strip") == 0;
@@ -1011,7 +1020,7 @@ pirk_status run_large(pirk_ctx* ctx, const pirk_model* m, int method, const pirk
         }();
         if (pipelined && is_heat(m) && method == PIRK_METHOD_MM && ss.size() == 1 && tube && tube->lower &&
             tube->upper && tube->max_slots >= 1 && m->dim >= (1ull << 22) && !exact_mode(ctx) &&
-            m->grid % 2 == 0 && heat_single_field_ok())
+            m->grid % 2 == 0 && heat_single_field_ok() && heat_plan_strip_ok(m, p, pl))
             return run_heat_mm_pipelined(ctx, m, p, tube, rep);
     }
     const auto t_setup = Clock::now();

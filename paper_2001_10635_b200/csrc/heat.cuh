@@ -76,7 +76,35 @@ struct HeatStepParams {
     // fast-mode Horner coefficients hk*kk/4, /3, /2, /1 (heat2x2.cuh): for a
     // linear autonomous field RK4 is x + hL(x + hL/2(x + hL/3(x + hL/4 x)))
     double hn[4];
+    // fast-mode strip kernel (heat_strip.cuh PIRK_STRIP_SFORM): RK4 of the
+    // linear field as a polynomial in the neighbour-sum operator S (L = S - 6),
+    // P(z(S - 6)) = q0 + q1 S + .. + q4 S^4, z = hk*kk, evaluated as
+    // w1 = S x + sf[0] x, w2 = S w1 + sf[1] x, w3 = S w2 + sf[2] x,
+    // y = sf[3] S w3 + sf[4] x  (sf = q3/q4, q2/q4, q1/q4, q4, q0)
+    double sf[5];
 };
+
+// S-form coefficients for z = hk*kk (host).  Returns false when z is outside
+// the range the strip kernel's S form is used for: its stage values grow like
+// |w3| ~ 24/z^3 |x|, so tiny z (the remainder step of a plan, very small h)
+// runs the Horner-in-L kernels instead.
+inline bool heat_sform_coeffs(double z, double* sf) {
+    if (!(z >= 1e-6) || !(z < 1e6)) return false;
+    const long double Z = z, Z2 = Z * Z, Z3 = Z2 * Z, Z4 = Z3 * Z;
+    const long double q4 = Z4 / 24.0L;
+    const long double q3 = Z3 * (1.0L - 6.0L * Z) / 6.0L;
+    const long double q2 = Z2 * (1.0L - 6.0L * Z + 18.0L * Z2) / 2.0L;
+    const long double q1 = Z * (1.0L - 6.0L * Z + 18.0L * Z2 - 36.0L * Z3);
+    const long double q0 = 1.0L - 6.0L * Z + 18.0L * Z2 - 36.0L * Z3 + 54.0L * Z4;
+    if (sf) {
+        sf[0] = static_cast<double>(q3 / q4);
+        sf[1] = static_cast<double>(q2 / q4);
+        sf[2] = static_cast<double>(q1 / q4);
+        sf[3] = static_cast<double>(q4);
+        sf[4] = static_cast<double>(q0);
+    }
+    return true;
+}
 
 // face flags (edge tiles); kOdd marks an odd footprint column (neighbour offsets)
 enum : int { kXm = 1, kXp = 2, kYm = 4, kYp = 8, kIn = 16, kOdd = 32 };

@@ -645,7 +645,9 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
     }();
     // one-field launches exist for the strip kernel only (fast mode, even g);
     // the engine's field-pipelined driver checks that before using them
-    if (field_only >= 0 && (Exact || variant != 3 || m.g % 2 != 0)) return cudaErrorInvalidValue;
+    if (field_only >= 0 && (Exact || variant != 3 || m.g % 2 != 0 ||
+                            (PIRK_STRIP_SFORM && !heat_sform_coeffs(sc.hk * m.kk, nullptr))))
+        return cudaErrorInvalidValue;
 
     // dynamic shared memory opt-in is per device: once per kernel and device
     static std::atomic<unsigned long long> attr_done{0};
@@ -690,7 +692,7 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
             cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
         return v > 0 ? v : 148;
     }();
-    HeatStepParams hp;
+    HeatStepParams hp{};
     hp.kk = m.kk;
     hp.robin = m.robin;
     hp.h2kk = sc.h2 * m.kk;
@@ -700,6 +702,8 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
     hp.hn[0] = hp.hn[3] / 4.0;
     hp.hn[1] = hp.hn[3] / 3.0;
     hp.hn[2] = hp.hn[3] / 2.0;
+    // the strip kernel's S form needs z = hk*kk in heat_sform_coeffs' range
+    const bool sform_ok = !PIRK_STRIP_SFORM || heat_sform_coeffs(sc.hk * m.kk, hp.sf);
     const uint64_t planes = w.out_end - w.out_begin;
     const uint64_t wplanes = w.win_end - w.win_begin;
     const bool vec = (m.g % 2 == 0) && reinterpret_cast<uintptr_t>(w.out0) % 16 == 0 &&
@@ -707,7 +711,7 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
     HeatTmaps tm;
     std::memset(&tm, 0, sizeof tm);
     if constexpr (!Exact) {
-        if (variant == 3 && heat_encode_tmap(&tm.f[0], w.in0, m.g, wplanes, kSF, kSF) &&
+        if (variant == 3 && sform_ok && heat_encode_tmap(&tm.f[0], w.in0, m.g, wplanes, kSF, kSF) &&
             heat_encode_tmap(&tm.f[1], w.in1, m.g, wplanes, kSF, kSF)) {
             const uint64_t tx = (m.g + kST - 1) / kST;
             const uint64_t zchunk = heat_zchunk(tx, planes, n_sm, nf);

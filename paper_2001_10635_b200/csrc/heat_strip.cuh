@@ -88,6 +88,17 @@
 // hazard would be a real one.
 #define PIRK_STRIP_SANITIZE 0
 #endif
+#ifndef PIRK_STRIP_SFORM
+// 1: RK4 as a polynomial in the neighbour-sum operator S (HeatStepParams::sf):
+// a stage is w = S(v) + a x, one DFMA instead of Horner-in-L's two
+// (x + c (S(v) - 6 v)); stage 4 is y = q4 S(w3) + q0 x
+#define PIRK_STRIP_SFORM 1
+#endif
+#ifndef PIRK_STRIP_F32CHK
+// 1: the per-block non-finite screen sums the values' high words on the FP32
+// pipe (common.cuh maybe_nonfinite8) instead of 7 DADDs on the FP64 pipe
+#define PIRK_STRIP_F32CHK 1
+#endif
 #ifndef PIRK_STRIP_S4SKIP
 #define PIRK_STRIP_S4SKIP 0  // halo warps 0 and 15 skip stage 4 (measured slower: 7.40 vs 6.55 ms, g=800)
 #endif
@@ -165,6 +176,16 @@ struct HeatStrip {
     double xc[8];  // XCARRY: own block of x(j) for the next iteration (valid after any iteration)
 
     __device__ __forceinline__ unsigned ts(int slot) const { return tt + 16u * slot; }
+    // stage coefficient s (0..2) and stage 4's S coefficient
+    __device__ __forceinline__ double cst(int s) const { return PIRK_STRIP_SFORM ? hp.sf[s] : hp.hn[s]; }
+    __device__ __forceinline__ double c4() const { return PIRK_STRIP_SFORM ? hp.sf[3] : hp.hn[3]; }
+    // A4(p) from u3(p-1), u3(p), x(p)
+    __device__ __forceinline__ double a4_of(double um, double u, double x) const {
+        if constexpr (PIRK_STRIP_SFORM)
+            return fma(hp.sf[3], um, hp.sf[4] * x);
+        else
+            return fma(hp.hn[3], fma(-6.0, u, um), x);
+    }
     __device__ __forceinline__ double* xslot(int s) const { return XR + s * kSXSlot; }
 
 #ifndef PIRK_STRIP_ST2
@@ -310,14 +331,20 @@ struct HeatStrip {
         }
     }
 
-    // o = base + cs (inplane + zm + zp - 6 C)
+    // Horner in L: o = base + cs (inplane + zm + zp - 6 C)
+    // S form:      o = (inplane + zm + zp) + cs base
     __device__ __forceinline__ void stage(const double (&C)[8], const double (&T)[2], const double (&B)[2],
                                           const double (&zm)[8], const double (&zp)[8], const double (&bs)[8],
                                           double cs, double (&o)[8]) const {
         double s[8];
         inplane(C, T, B, s);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = fma(cs, fma(-6.0, C[i], s[i] + (zm[i] + zp[i])), bs[i]);
+        for (int i = 0; i < 8; ++i) {
+            if constexpr (PIRK_STRIP_SFORM)
+                o[i] = fma(cs, bs[i], s[i] + (zm[i] + zp[i]));
+            else
+                o[i] = fma(cs, fma(-6.0, C[i], s[i] + (zm[i] + zp[i])), bs[i]);
+        }
     }
 
     // One plane of the pipeline.  edge: the iteration touches a chunk edge or
@@ -392,7 +419,7 @@ struct HeatStrip {
                 for (int i = 0; i < 8; ++i) zm[i] = C[i];
             }
             x_tb(Xm, T, B);
-            stage(C, T, B, zm, zp, C, hp.hn[0], o1);
+            stage(C, T, B, zm, zp, C, cst(0), o1);
             st8(ts(U1B), o1);  // u1(j-1) replaces u1(j-3)
             wait_prev();  // every warp is past the previous plane's exchange reads
             publish(PH, 0, o1);
@@ -422,7 +449,7 @@ struct HeatStrip {
                 for (int i = 0; i < 8; ++i) o1[i] = C[i];
             }
             u_tb(PH ^ 1, 0, T, B);
-            stage(C, T, B, zm2, o1, bs, hp.hn[1], o2);
+            stage(C, T, B, zm2, o1, bs, cst(1), o2);
             st8(ts(U2B), o2);  // u2(j-2) replaces u2(j-4)
             if (PIRK_STRIP_LADDER) wait_bar(2);
             publish(PH, 1, o2);
@@ -453,7 +480,7 @@ struct HeatStrip {
                 for (int i = 0; i < 8; ++i) o2[i] = C[i];
             }
             u_tb(PH ^ 1, 1, T, B);
-            stage(C, T, B, zm3, o2, bs, hp.hn[2], o3);
+            stage(C, T, B, zm3, o2, bs, cst(2), o3);
             if (inner) st8(ts(kSU3), o3);  // u3(j-3) replaces u3(j-4)
             if (PIRK_STRIP_LADDER) wait_bar(0);
             publish(PH, 2, o3);
@@ -466,7 +493,7 @@ struct HeatStrip {
                 if (a4) {
                     double an[8];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) an[i] = fma(hp.hn[3], fma(-6.0, o3[i], C4[i]), bs[i]);
+                    for (int i = 0; i < 8; ++i) an[i] = a4_of(C4[i], o3[i], bs[i]);
                     st8(ts(kSA4), an);
                 }
             }
@@ -498,7 +525,7 @@ struct HeatStrip {
                 u_tb(PH ^ 1, 2, T, B);
                 inplane(C4, T, B, s);
 #pragma unroll
-                for (int i = 0; i < 8; ++i) y[i] = fma(hp.hn[3], s[i] + o3[i], av[i]);
+                for (int i = 0; i < 8; ++i) y[i] = fma(c4(), s[i] + o3[i], av[i]);
                 if (st_own) {
 #pragma unroll
                     for (int r = 0; r < 4; ++r)
@@ -522,14 +549,15 @@ struct HeatStrip {
                     }
                 }
                 if ((st_own || st_mask) &&
-                    !finite_d(((y[0] + y[1]) + (y[2] + y[3])) + ((y[4] + y[5]) + (y[6] + y[7]))))
+                    (PIRK_STRIP_F32CHK ? maybe_nonfinite8(y)
+                                       : !finite_d(((y[0] + y[1]) + (y[2] + y[3])) + ((y[4] + y[5]) + (y[6] + y[7])))))
                     heat_strip_report(stp, g, g2, j - 4, gout, st_own ? 0xffu : st_mask, field, method, step,
                                       fail, n_total);
             }
             if (!PIRK_STRIP_XSWAP && a4) {
                 double an[8];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) an[i] = fma(hp.hn[3], fma(-6.0, o3[i], C4[i]), x3[i]);
+                for (int i = 0; i < 8; ++i) an[i] = a4_of(C4[i], o3[i], x3[i]);
                 st8(ts(kSA4), an);
             }
         }

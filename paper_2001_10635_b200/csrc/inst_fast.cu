@@ -6,6 +6,10 @@
 
 namespace pirk {
 
+bool heat_strip_step_ok(const HeatModel& m, double hk) {
+    return !PIRK_STRIP_SFORM || heat_sform_coeffs(hk * m.kk, nullptr);
+}
+
 template cudaError_t launch_chain_step<false>(const ChainModel&, const WindowArgs&,
                                               const StepConsts&, unsigned long long,
                                               unsigned long long*, cudaStream_t);

@@ -90,6 +90,10 @@ template <bool Exact>
 cudaError_t launch_chain_steps(const ChainModel& m, const WindowArgs& w, const StepConstsN& scs, int S,
                                unsigned long long step, unsigned long long* fail, cudaStream_t stream);
 
+// Fast mode: whether a step of length hk can run the strip kernel (and so a
+// one-field launch, field_only >= 0); defined in inst_fast.cu.
+bool heat_strip_step_ok(const HeatModel& m, double hk);
+
 template <bool Exact>
 cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const StepConsts& sc,
                              unsigned long long step, unsigned long long* fail,

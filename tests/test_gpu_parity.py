@@ -134,6 +134,42 @@ def test_heat_fast_mode_long_run(fast_ctx):
     assert_within(pk.growth_bound(prob, ctx=fast_ctx), oracle_for("gb", prob))
 
 
+@pytest.mark.parametrize("z", [1.0 / 6.0, 0.02, 2e-6])
+def test_heat_fast_sform_z_range(fast_ctx, z):
+    """The strip kernel evaluates RK4 as a polynomial in the neighbour-sum
+    operator S (heat.cuh heat_sform_coeffs); its stage coefficients are
+    q3/q4, q2/q4, q1/q4.  z = h*kk = 1/6 is the root of q3 (a Horner form in S
+    with q_k/q_{k+1} coefficients would divide by zero there); 2e-6 is near
+    the small-z limit of the S form (stage values ~24/z^3 |x|)."""
+    g = 72
+    n = g ** 3
+    rng = np.random.default_rng(21)
+    lo = rng.uniform(0.5, 1.0, n)
+    hi = lo + rng.uniform(0.0, 0.5, n)
+    h = z / (g - 1) ** 2
+    m, prob = heat_problem(g, t1=6 * h, h=h, stride=2, lo=lo, hi=hi)
+    assert_within(pk.mixed_monotonicity(prob, ctx=fast_ctx), oracle_for("mm", prob))
+
+
+@pytest.mark.parametrize("g", [72, 162])
+def test_heat_fast_tiny_remainder_step(fast_ctx, g):
+    """A remainder step with z = hk*kk far below the S form's range runs the
+    Horner-in-L kernel for that step (launch_heat_step); g = 162 (n >= 2^22,
+    final box only) is the field-pipelined driver's case, which then takes the
+    per-step path (engine.cu heat_plan_strip_ok)."""
+    n = g ** 3
+    rng = np.random.default_rng(23)
+    lo = rng.uniform(0.5, 1.0, n)
+    hi = lo + rng.uniform(0.0, 0.5, n)
+    h = 0.2 / (g - 1) ** 2
+    t1 = 3 * h + 1e-7 * h
+    stride = 0 if g == 162 else 1
+    m, prob = heat_problem(g, t1=t1, h=h, stride=stride, lo=lo, hi=hi)
+    ref = oracle_for("mm", prob)
+    assert len(ref.times) == (1 if stride == 0 else 5)
+    assert_within(pk.mixed_monotonicity(prob, ctx=fast_ctx), ref)
+
+
 @pytest.mark.parametrize("variant", ["1x2", "2x2", "strip"])
 def test_heat_block_variants(variant):
     """Both heat kernels (1x2 pairs, 2x2 blocks) in both modes: the selector
