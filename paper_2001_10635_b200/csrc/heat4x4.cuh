@@ -65,6 +65,9 @@
 
 #include "heat.cuh"
 #include "tmem_io.cuh"
+#if !PIRK_TM_LD_WAITST
+#error "heat4x4.cuh relies on per-load store waits: build dev variants with -DPIRK_TM_LD_WAITST=1"
+#endif
 
 namespace pirk {
 

@@ -99,6 +99,11 @@
 // pipe (common.cuh maybe_nonfinite8) instead of 7 DADDs on the FP64 pipe
 #define PIRK_STRIP_F32CHK 1
 #endif
+#ifndef PIRK_STRIP_EARLYLD
+// 1: steady-state iterations issue stage 1's three TMEM loads (x(j-3), x(j-2),
+// u1(j-3)) before the x-plane wait and complete them just before use
+#define PIRK_STRIP_EARLYLD 0
+#endif
 #ifndef PIRK_STRIP_S4SKIP
 #define PIRK_STRIP_S4SKIP 0  // halo warps 0 and 15 skip stage 4 (measured slower: 7.40 vs 6.55 ms, g=800)
 #endif
@@ -363,6 +368,9 @@ struct HeatStrip {
         const bool has_x = !edge || j < ze;
 
         if constexpr (!PIRK_TM_LD_WAITST) tm_wait_st();  // the previous plane's TMEM stores land before its slots are read
+        const bool early = PIRK_STRIP_EARLYLD && PIRK_STRIP_XSWAP && !edge;
+        unsigned er[48];
+        if (early) tm_ld8x3_issue(ts(XB), ts(XA), ts(U1B), er);
         // ---- x(j): wait for its box; prefetch x(j+2) into the slot of x(j-2)
         const double* Xj = xslot(xs);
         const double* Xm = xslot((xs + 3) & 3);  // x(j-1)
@@ -399,11 +407,19 @@ struct HeatStrip {
             } else {
                 own_x(Xm, C);
             }
-            if constexpr (PIRK_STRIP_XSWAP) {
-                tm_ld8(ts(XB), xb);
+            if (early) {
+                tm_ld_wait48(er);
+                tm_unpack8(er, xb);
+                tm_unpack8(er + 16, zm);
+                tm_unpack8(er + 32, zm2);
                 st8(ts(XB), C);  // x(j-1) replaces x(j-3)
+            } else {
+                if constexpr (PIRK_STRIP_XSWAP) {
+                    tm_ld8(ts(XB), xb);
+                    st8(ts(XB), C);  // x(j-1) replaces x(j-3)
+                }
+                tm_ld8x2(ts(XA), ts(U1B), zm, zm2);  // x(j-2); u1(j-3) before it is overwritten
             }
-            tm_ld8x2(ts(XA), ts(U1B), zm, zm2);  // x(j-2); u1(j-3) before it is overwritten
             if (!edge || j < g) {
                 own_x(Xj, zp);
             } else {  // x(g) := x(g-1)
