@@ -603,7 +603,7 @@ heat2_step_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
 // z-chunk length for one-CTA-per-SM heat kernels over tx x tx tiles and two
 // fields: the count minimising waves x (planes per chunk + 8 halo planes
 // recomputed per chunk), i.e. the wave quantisation of nf tx^2 CTAs per chunk
-inline uint64_t heat_zchunk_tiles(uint64_t tiles, uint64_t planes, int n_sm, unsigned nf = 2) {
+inline uint64_t heat_zchunk(uint64_t tx, uint64_t planes, int n_sm, unsigned nf = 2) {
     static const int forced = [] {  // PIRK_HEAT_ZCHUNKS=c forces c chunks (A/B only)
         const char* v = std::getenv("PIRK_HEAT_ZCHUNKS");
         return v ? std::atoi(v) : 0;
@@ -613,15 +613,12 @@ inline uint64_t heat_zchunk_tiles(uint64_t tiles, uint64_t planes, int n_sm, uns
     double best_cost = 0.0;
     for (uint64_t c = 1; c <= 8 && c <= planes; ++c) {
         const uint64_t zc = (planes + c - 1) / c;
-        const uint64_t ctas = tiles * nf * ((planes + zc - 1) / zc);
+        const uint64_t ctas = tx * tx * nf * ((planes + zc - 1) / zc);
         const double cost = static_cast<double>((ctas + n_sm - 1) / n_sm) *
                             static_cast<double>(zc + (c > 1 ? 2 * kHeatH : 0));
         if (c == 1 || cost < best_cost) best = c, best_cost = cost;
     }
     return (planes + best - 1) / best;
-}
-inline uint64_t heat_zchunk(uint64_t tx, uint64_t planes, int n_sm, unsigned nf = 2) {
-    return heat_zchunk_tiles(tx * tx, planes, n_sm, nf);
 }
 
 template <bool Exact>
@@ -683,14 +680,6 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
                 e = cudaFuncSetAttribute(heat_strip_kernel<Exact, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSSmemBytes));
             if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(heat_strip_kernel<Exact, false, false, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSSmemBytesPair));
-            if (e == cudaSuccess)
-                e = cudaFuncSetAttribute(heat_strip_kernel<Exact, true, false, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSSmemBytesPair));
-            if (e == cudaSuccess)
                 e = cudaFuncSetAttribute(heat_strip_kernel<Exact, false, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSSmemBytes));
         }
@@ -722,44 +711,9 @@ cudaError_t launch_heat_step(const HeatModel& m, const WindowArgs& w, const Step
     HeatTmaps tm;
     std::memset(&tm, 0, sizeof tm);
     if constexpr (!Exact) {
-        // y-pair clusters (heat_strip.cuh HeatStrip Pair): 60 output rows per
-        // CTA instead of 56, so fewer CTAs; PIRK_STRIP_PAIR=0 turns them off
-        // (A/B).  Peer-store (mirrored) windows keep single tiles.
-        static const bool pair_on = [] {
-            const char* v = std::getenv("PIRK_STRIP_PAIR");
-            return !(v && std::strcmp(v, "0") == 0);
-        }();
-        const bool pair = pair_on && !w.mirrored();
-        const unsigned box_y = pair ? kSF + 1 : kSF;
-        if (variant == 3 && sform_ok && heat_encode_tmap(&tm.f[0], w.in0, m.g, wplanes, kSF, box_y) &&
-            heat_encode_tmap(&tm.f[1], w.in1, m.g, wplanes, kSF, box_y)) {
+        if (variant == 3 && sform_ok && heat_encode_tmap(&tm.f[0], w.in0, m.g, wplanes, kSF, kSF) &&
+            heat_encode_tmap(&tm.f[1], w.in1, m.g, wplanes, kSF, kSF)) {
             const uint64_t tx = (m.g + kST - 1) / kST;
-            if (pair) {
-                const uint64_t npairs = (m.g + kSPairOut - 1) / kSPairOut;
-                const uint64_t ty = 2 * npairs;
-                const uint64_t ty_live = ty - ((npairs - 1) * kSPairOut + kSPairOut / 2 >= m.g ? 1 : 0);
-                const uint64_t zchunk = heat_zchunk_tiles(tx * ty_live, planes, n_sm, nf);
-                const uint64_t nchunks = (planes + zchunk - 1) / zchunk;
-                cudaLaunchConfig_t cfg{};
-                cfg.gridDim = dim3(static_cast<unsigned>(tx), static_cast<unsigned>(ty),
-                                   static_cast<unsigned>(nf * nchunks));
-                cfg.blockDim = dim3(kSThreads, 1, 1);
-                cfg.dynamicSmemBytes = kSSmemBytesPair;
-                cfg.stream = stream;
-                cudaLaunchAttribute at[1];
-                at[0].id = cudaLaunchAttributeClusterDimension;
-                at[0].val.clusterDim.x = 1;
-                at[0].val.clusterDim.y = 2;
-                at[0].val.clusterDim.z = 1;
-                cfg.attrs = at;
-                cfg.numAttrs = 1;
-                const int flags = 1 | (vec ? 2 : 0) | (field_only >= 0 ? fsel : 0);
-                if (field_only >= 0)
-                    return cudaLaunchKernelEx(&cfg, heat_strip_kernel<Exact, true, false, true>, m, hp, w, sc, step,
-                                              zchunk, fail, tm, flags);
-                return cudaLaunchKernelEx(&cfg, heat_strip_kernel<Exact, false, false, true>, m, hp, w, sc, step,
-                                          zchunk, fail, tm, flags);
-            }
             const uint64_t zchunk = heat_zchunk(tx, planes, n_sm, nf);
             const uint64_t nchunks = (planes + zchunk - 1) / zchunk;
             dim3 grid(static_cast<unsigned>(tx), static_cast<unsigned>(tx), static_cast<unsigned>(nf * nchunks));

@@ -121,41 +121,6 @@ constexpr size_t kSRingBytes = size_t(kSXSlots) * kSXSlot * sizeof(double);    /
 // [exchange][x ring][one row of padding]: the rows above / below the
 // footprint that halo blocks read land in the exchange region or the padding
 constexpr size_t kSSmemBytes = kSEdgeBytes + kSRingBytes + kSF * sizeof(double);
-// y-pair clusters (PIRK_STRIP_PAIR, below): 65-row x boxes, one row beyond the
-// footprint on the pair's shared side
-constexpr int kSPairOut = 120;                                  // output rows of a pair (60 + 60)
-constexpr int kSXSlotPair = kSF * (kSF + 1);
-constexpr size_t kSSmemBytesPair = kSEdgeBytes + size_t(kSXSlots) * kSXSlotPair * sizeof(double) + kSF * sizeof(double);
-static_assert(kSSmemBytesPair + 256 <= 232448, "pair variant exceeds the 227 KB shared-memory opt-in");
-
-// ---- thread-block cluster helpers (y-pair variant)
-__device__ __forceinline__ unsigned cluster_ctarank() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ unsigned mapa_shared(unsigned addr, unsigned rank) {
-    unsigned r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void st_cluster_d2(unsigned addr, double a, double b) {
-    asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};\n" ::"r"(addr), "d"(a), "d"(b) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(unsigned addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(addr) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_acq_cluster(unsigned long long* b, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred p;\nPIRK_CWAIT_%=:\n"
-        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra PIRK_CWAIT_%=;\n}\n" ::"r"(smem_u32(b)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
 
 // TMEM plane slots of a thread (16 columns = 8 doubles each)
 enum : int { kSX = 0, kSU1 = 2, kSU2 = 4, kSU3 = 6, kSA4 = 7 };
@@ -182,19 +147,8 @@ __device__ __forceinline__ void heat_strip_report(const double* stp, int g, long
 
 // Kind: 0 interior tile, 1 edge tile of a g % 4 == 0 grid (PIRK_STRIP_EDGECSE),
 // 2 any other edge tile
-// Pair: the CTA is one of a y-pair cluster (PIRK_STRIP_PAIR).  The pair's two
-// 64-row footprints abut: the top CTA owns rows [y0-4, y0+60) and stores rows
-// y0 .. y0+59 (warps 1..15), the bottom CTA owns [y0+60, y0+124) and stores
-// y0+60 .. y0+119 (warps 0..14).  Neither recomputes a halo on the shared side:
-// the top CTA's warp 15 and the bottom CTA's warp 0 exchange their boundary
-// rows of each level through distributed shared memory (stored into the
-// peer's exchange slots that no local warp uses: the top CTA's warp-0 TOP, the
-// bottom CTA's warp-15 BOT), and arrive on the peer's per-plane barrier, so
-// the split barrier orders the remote rows exactly as it orders local ones.
-// Stage 1's x row across the seam comes from a 65-row TMA box.
-template <int Kind, bool Mirror = false, bool Pair = false>
+template <int Kind, bool Mirror = false>
 struct HeatStrip {
-    static constexpr int kSlot = Pair ? kSXSlotPair : kSXSlot;
     static constexpr bool Interior = Kind == 0;
     static constexpr bool EdgeCse = Kind == 1;
     const HeatStepParams& hp;
@@ -222,13 +176,6 @@ struct HeatStrip {
     unsigned long long* bars;
     unsigned long long* done;  // split barrier: warps arrive when a plane's exchange work is complete
     unsigned tt;  // TMEM address of slot 0
-    // Pair: u_tb offsets (double2 units within a level), publish redirections
-    int ua_off, uc_off;
-    bool skip_top, skip_bot;  // the slot is the peer's (top CTA warp 0 TOP / bottom CTA warp 15 BOT)
-    unsigned rpub;            // boundary warp with a live peer: peer's exchange base (cluster address), else 0
-    int rpub_idx;             // double2 index within a level of the remote store
-    bool rpub_top;            // remote store is the block's TOP row (bottom CTA) or BOT row (top CTA)
-    unsigned rdone;           // peer's done barrier (cluster address), boundary warps with a live peer
     int xs;       // x ring slot of plane j
     int xph;      // mbarrier phase bit per slot
     double xc[8];  // XCARRY: own block of x(j) for the next iteration (valid after any iteration)
@@ -244,7 +191,7 @@ struct HeatStrip {
         else
             return fma(hp.hn[3], fma(-6.0, u, um), x);
     }
-    __device__ __forceinline__ double* xslot(int s) const { return XR + s * kSlot; }
+    __device__ __forceinline__ double* xslot(int s) const { return XR + s * kSXSlot; }
 
 #ifndef PIRK_STRIP_ST2
 #define PIRK_STRIP_ST2 1
@@ -261,7 +208,7 @@ struct HeatStrip {
     }
 
     __device__ __forceinline__ void tma(int p, int s) {
-        mbar_expect_tx(bars + s, kSlot * sizeof(double));
+        mbar_expect_tx(bars + s, kSXSlot * sizeof(double));
         tma_load_plane(xslot(s), tmap, bx0, by0, p - wbz, bars + s);
     }
 
@@ -277,7 +224,7 @@ struct HeatStrip {
 
     // rows above / below the block: from the x slot (stage 1) or a level
     __device__ __forceinline__ const double* dummy_row() const {
-        return XR + kSXSlots * kSlot + 2 * (t & 31);  // the padding row after the ring
+        return XR + kSXSlots * kSXSlot + 2 * (t & 31);  // the padding row after the ring
     }
     __device__ __forceinline__ void x_tb(const double* X, double (&T)[2], double (&B)[2]) const {
         const double* pa = X + xo - kSF;
@@ -293,9 +240,9 @@ struct HeatStrip {
     // exchange buffer `buf` (iteration parity) of level 0..2 (u1..u3)
     __device__ __forceinline__ void u_tb(int buf, int level, double (&T)[2], double (&B)[2]) const {
         const double2* L = EX + (3 * buf + level) * kSLevel;
-        const double2* pa = L + (Pair ? ua_off : kSThreads + t - 32);  // BOT of the block above
-        const double2* pc = L + (Pair ? uc_off : t + 32);              // TOP of the block below
-        if constexpr (PIRK_STRIP_SANITIZE && !Pair) {
+        const double2* pa = L + kSThreads + t - 32;  // BOT of the block above
+        const double2* pc = L + t + 32;              // TOP of the block below
+        if constexpr (PIRK_STRIP_SANITIZE) {
             if (t < 32) pa = reinterpret_cast<const double2*>(dummy_row());
             if (t >= kSThreads - 32) pc = reinterpret_cast<const double2*>(dummy_row());
         }
@@ -305,16 +252,8 @@ struct HeatStrip {
     }
     __device__ __forceinline__ void publish(int buf, int level, const double (&v)[8]) const {
         double2* L = EX + (3 * buf + level) * kSLevel;
-        if constexpr (Pair) {
-            if (!skip_top) L[t] = make_double2(v[0], v[1]);
-            if (!skip_bot) L[kSThreads + t] = make_double2(v[6], v[7]);
-            if (rpub)
-                st_cluster_d2(rpub + static_cast<unsigned>(((3 * buf + level) * kSLevel + rpub_idx) * sizeof(double2)),
-                              rpub_top ? v[0] : v[6], rpub_top ? v[1] : v[7]);
-        } else {
-            L[t] = make_double2(v[0], v[1]);
-            L[kSThreads + t] = make_double2(v[6], v[7]);
-        }
+        L[t] = make_double2(v[0], v[1]);
+        L[kSThreads + t] = make_double2(v[6], v[7]);
     }
 
     // anti-diagonal pair sums P(r, c) = v(r, c+1) + v(r+1, c) are shared:
@@ -440,26 +379,10 @@ struct HeatStrip {
         // level 1 / level 2 of a plane, so a fast warp waits only for the
         // exchange rows it is about to overwrite)
         auto wait_bar = [&](int b) {
-            if (PIRK_STRIP_SPLITBAR && j > zs) {
-                if constexpr (Pair)
-                    mbar_wait_acq_cluster(done + b, static_cast<unsigned>(j - 1 - zs) & 1u);
-                else
-                    mbar_wait(done + b, static_cast<unsigned>(j - 1 - zs) & 1u);
-            }
+            if (PIRK_STRIP_SPLITBAR && j > zs) mbar_wait(done + b, static_cast<unsigned>(j - 1 - zs) & 1u);
         };
         auto wait_prev = [&]() { wait_bar(PIRK_STRIP_LADDER ? 1 : 0); };
         auto arrive = [&](int b) {
-            if constexpr (Pair) {
-                if (rdone) {  // boundary warp: this plane's remote rows are visible before the peer's arrival
-                    asm volatile("fence.acq_rel.cluster;\n" ::: "memory");
-                    __syncwarp();
-                    if ((threadIdx.x & 31) == 0) {
-                        mbar_arrive(done + b);
-                        mbar_arrive_remote(rdone + static_cast<unsigned>(b * sizeof(unsigned long long)));
-                    }
-                    return;
-                }
-            }
             __syncwarp();
             if ((threadIdx.x & 31) == 0) mbar_arrive(done + b);
         };
@@ -712,7 +635,7 @@ struct HeatStrip {
     }
 };
 
-template <bool Exact, bool One = false, bool Mirror = false, bool Pair = false>
+template <bool Exact, bool One = false, bool Mirror = false>
 __global__ void __launch_bounds__(kSThreads, 1)
 heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w, const StepConsts sc,
                   const unsigned long long step, const uint64_t zchunk,
@@ -732,31 +655,17 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
     const int field = One ? ((flags >> 3) & 1) : static_cast<int>(blockIdx.z & 1);
     const long long chunk = One ? static_cast<long long>(blockIdx.z) : static_cast<long long>(blockIdx.z >> 1);
     const long long ix0 = static_cast<long long>(blockIdx.x) * kST;
-    // footprint origin in y (kHeatH rows above the first output row of a
-    // single tile); Pair: see HeatStrip
-    unsigned prank = 0;
-    bool peer = false;
-    long long foy = static_cast<long long>(blockIdx.y) * kST - kHeatH;
-    if constexpr (Pair) {
-        prank = cluster_ctarank();
-        const long long py0 = static_cast<long long>(blockIdx.y >> 1) * kSPairOut;
-        peer = py0 + kSPairOut / 2 < g;  // the bottom CTA has rows inside the grid
-        if (prank == 1 && !peer) return;  // (its top CTA then never touches it)
-        foy = prank ? py0 + kSPairOut / 2 : py0 - kHeatH;
-    }
+    const long long iy0 = static_cast<long long>(blockIdx.y) * kST;
     const long long obz = static_cast<long long>(w.out_begin) + chunk * static_cast<long long>(zchunk);
     long long oez = obz + static_cast<long long>(zchunk);
     if (oez > static_cast<long long>(w.out_end)) oez = static_cast<long long>(w.out_end);
     if (obz >= oez) return;
 
     const int warp = tid >> 5, lane = tid & 31;
-    const long long gx0 = ix0 - kHeatH + 2 * lane, gy0 = foy + 4 * warp;
-    const bool own = lane >= 2 && lane <= 29 &&
-                     (Pair ? (prank ? warp <= 14 : warp >= 1) : (warp >= 1 && warp <= 14));
-    // Pair top CTA: its last rows are outputs, so a y = g-1 face anywhere in the
-    // footprint makes it an edge tile
-    const bool interior = ix0 - kHeatH >= 0 && ix0 + kST + kHeatH <= g && foy >= 0 &&
-                          foy + kSF + ((Pair && prank == 0) ? 1 : 0) <= g;
+    const long long gx0 = ix0 - kHeatH + 2 * lane, gy0 = iy0 - kHeatH + 4 * warp;
+    const bool own = lane >= 2 && lane <= 29 && warp >= 1 && warp <= 14;
+    const bool interior = ix0 - kHeatH >= 0 && ix0 + kST + kHeatH <= g && iy0 - kHeatH >= 0 &&
+                          iy0 + kST + kHeatH <= g;
     unsigned st_mask = 0;
     int fx0 = 0, fxg = 0, fy0 = 0, fyg = 0;
     for (int c = 0; c < 2; ++c) {
@@ -788,15 +697,12 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
     if (warp == 0) tmem_alloc512(&tmem_base);
     if (tid == 0) {
         for (int s = 0; s < kSXSlots; ++s) mbar_init(bars + s, 1);
-        for (int b = 0; b < 3; ++b) mbar_init(done_bar + b, kSThreads / 32 + (Pair && peer ? 1 : 0));
+        for (int b = 0; b < 3; ++b) mbar_init(done_bar + b, kSThreads / 32);
         mbar_fence_init();
     }
     tmem_fence_before();
     __syncthreads();
     tmem_fence_after();
-    if constexpr (Pair) {
-        if (peer) cluster_sync_all();  // the peer's barriers are initialised before any remote arrive
-    }
     // warp w: TMEM lane quadrant w % 4, columns 128 (w / 4) .. +127 (8 slots of 16)
     // (through a warp reduction: its result lives in a uniform register, so the
     // TMEM addresses of the loop's tcgen05 ops need no per-use R2UR)
@@ -804,12 +710,12 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
                                                           static_cast<unsigned>(128 * (warp >> 2)));
 #define PIRK_STRIP_RUN(INTERIOR)                                                                     \
     {                                                                                                \
-        HeatStrip<INTERIOR, Mirror, Pair> r{hp};                                                     \
+        HeatStrip<INTERIOR, Mirror> r{hp};                                                           \
         r.EX = reinterpret_cast<double2*>(smem);                                                     \
         r.XR = smem + kSEdgeBytes / sizeof(double);                                                  \
         r.t = tid;                                                                                   \
         r.inner = !PIRK_STRIP_S4SKIP || (warp >= 1 && warp <= 14);                                   \
-        r.xo = 4 * warp * kSF + 2 * lane + ((Pair && prank) ? kSF : 0);                              \
+        r.xo = 4 * warp * kSF + 2 * lane;                                                            \
         r.zs = zs, r.ze = ze, r.ob = static_cast<int>(obz), r.oe = static_cast<int>(oez);           \
         r.g = static_cast<int>(g), r.lo_shift = zs > 0, r.hi_shift = ze < g;                         \
         r.g2 = g2;                                                                                   \
@@ -825,20 +731,7 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
         r.field = field, r.method = m.method, r.step = step, r.fail = fail;                          \
         r.n_total = static_cast<unsigned long long>(g2 * g);                                         \
         r.tmap = &tm.f[field];                                                                       \
-        r.bx0 = static_cast<int>(ix0) - kHeatH, r.by0 = static_cast<int>(foy) - ((Pair && prank) ? 1 : 0); \
-        if constexpr (Pair) {                                                                        \
-            r.ua_off = kSThreads + tid - 32, r.uc_off = tid + 32;                                    \
-            r.skip_top = prank == 0 && warp == 0, r.skip_bot = prank == 1 && warp == 15;             \
-            r.rpub = 0, r.rpub_idx = 0, r.rpub_top = false, r.rdone = 0;                             \
-            if (prank == 0 && warp == 15) r.uc_off = lane;                                           \
-            if (prank == 1 && warp == 0) r.ua_off = kSThreads + 15 * 32 + lane;                      \
-            if (peer && ((prank == 0 && warp == 15) || (prank == 1 && warp == 0))) {                 \
-                r.rpub = mapa_shared(smem_u32(smem), prank ^ 1u);                                    \
-                r.rpub_top = prank == 1;                                                             \
-                r.rpub_idx = prank ? lane : kSThreads + 15 * 32 + lane;                              \
-                r.rdone = mapa_shared(smem_u32(done_bar), prank ^ 1u);                               \
-            }                                                                                        \
-        }                                                                                            \
+        r.bx0 = static_cast<int>(ix0) - kHeatH, r.by0 = static_cast<int>(iy0) - kHeatH;              \
         r.wbz = static_cast<int>(w.win_begin);                                                       \
         r.bars = bars;                                                                               \
         r.done = done_bar;                                                                           \
@@ -863,9 +756,6 @@ heat_strip_kernel(const HeatModel m, const HeatStepParams hp, const WindowArgs w
     __syncthreads();
     tmem_fence_after();
     if (warp == 0) tmem_dealloc512(tmem_base);
-    if constexpr (Pair) {
-        if (peer) cluster_sync_all();  // the peer's last remote rows / arrivals have landed before exit
-    }
 }
 
 }  // namespace pirk

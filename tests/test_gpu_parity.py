@@ -665,57 +665,6 @@ def test_heat_pipelined_skew_schedules_identical(tmp_path):
         assert np.max(np.abs(got - r) / np.abs(r)) <= 1e-12
 
 
-_PAIR_CHILD = r"""
-import sys, numpy as np, paper_2001_10635_b200 as pk
-g, steps, out = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
-n = g ** 3
-rng = np.random.default_rng(31)
-lo = rng.uniform(0.5, 1.0, n)
-hi = lo + rng.uniform(0.0, 0.5, n)
-h = 0.2 / (g - 1) ** 2
-m = pk.make_heat3d(g)
-prob = pk.ReachProblem(m, pk.IntervalVector(lo, hi), None, 0.0, steps * h, h, 1)
-c = pk.Context(0, "fast")
-t = pk.mixed_monotonicity(prob, ctx=c)
-np.save(out + "_lo.npy", np.stack([e.box.lower for e in t.entries]))
-np.save(out + "_hi.npy", np.stack([e.box.upper for e in t.entries]))
-"""
-
-
-@pytest.mark.parametrize("g", [124, 184, 242])
-def test_heat_strip_pair_clusters_identical(tmp_path, g):
-    """y-pair clusters (heat_strip.cuh Pair: two CTAs share their seam rows
-    through distributed shared memory instead of recomputing a halo) compute
-    every cell with the same expression as single tiles, so the results are
-    bit-identical with PIRK_STRIP_PAIR=0.  g = 124 and 242: the last pair's
-    bottom CTA lies outside the grid (it exits at once); 184: interior pair
-    tiles, the second pair's bottom CTA has 4 grid rows."""
-    import os, subprocess, sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = {}
-    for name, env in (("single", {"PIRK_STRIP_PAIR": "0"}), ("pair", {"PIRK_STRIP_PAIR": "1"})):
-        out = str(tmp_path / name)
-        r = subprocess.run([sys.executable, "-c", _PAIR_CHILD, str(g), "5", out],
-                           env=dict(os.environ, **env), cwd=root, capture_output=True, text=True, timeout=600)
-        assert r.returncode == 0, r.stderr[-3000:]
-        res[name] = (np.load(out + "_lo.npy"), np.load(out + "_hi.npy"))
-    assert np.array_equal(res["pair"][0], res["single"][0])
-    assert np.array_equal(res["pair"][1], res["single"][1])
-
-
-@pytest.mark.parametrize("g", [124, 184])
-def test_heat_strip_pair_vs_oracle(fast_ctx, g):
-    """The pair-cluster path (the default for even g) within the fast-mode
-    tolerance of the oracle, 4 steps."""
-    n = g ** 3
-    rng = np.random.default_rng(33)
-    lo = rng.uniform(0.5, 1.0, n)
-    hi = lo + rng.uniform(0.0, 0.5, n)
-    h = 0.2 / (g - 1) ** 2
-    m, prob = heat_problem(g, t1=4 * h, h=h, stride=2, lo=lo, hi=hi)
-    assert_within(pk.mixed_monotonicity(prob, ctx=fast_ctx), oracle_for("mm", prob))
-
-
 def test_small_serial_kernel_variant():
     """The one-thread small-system integrator (PIRK_SMALL_SERIAL=1) and the
     default warp-parallel one give the same results: the small-system tests
