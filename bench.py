@@ -440,6 +440,21 @@ def host_ram_gb():
     return vm.total / 2 ** 30, vm.available / 2 ** 30
 
 
+def host_cpu():
+    """CPU model and logical CPU count of this host (report them
+    beside the reference timing)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 def cpu_baseline(args):
     """The reference itself (oracle/_ref) on this host, bounded sample at the
     largest heat3d grid the host RAM holds (the reference keeps 7 vectors of
@@ -471,6 +486,7 @@ def cpu_baseline(args):
             "sample": f"ivreach::mixed_monotonicity (oracle/_ref, -O3, OpenMP, x86-64 baseline, no FMA) "
                       f"heat3d grid={g} (n={n}), {steps} RK4 steps, h={args.h}; rate = 2n*steps/integration_s; "
                       f"grid = the largest the host RAM holds (capped at {args.cpu_grid_max})",
+            **host_cpu(),
             "host_ram_gb": round(total_gb, 1), "host_ram_available_gb": round(avail_gb, 1),
             "reference_state_gb": round(112.0 * n / 1e9, 1),
             "wall_s": r.wall_s, "integration_s": r.report["integration_s"],
@@ -814,7 +830,7 @@ def run_reference(args):
             "config": {"workload": f"CTMM heat3d (bounded sample grid={g} of the grid={GRID} workload)",
                        "parallelism": f"openmp{threads}"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": sample},
+                             "sample": sample, **host_cpu()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
