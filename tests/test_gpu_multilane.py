@@ -111,6 +111,29 @@ def test_heat_zslab_lanes(g, lanes, mode):
         ck.close()
 
 
+def test_heat_lanes_tiny_remainder_step():
+    """Fast mode with a remainder step whose z = hk*kk is below the strip
+    kernel's S-form range: that step runs the Horner-in-L 2x2 kernel, in its
+    peer-store (Mirror) instantiation on 3 lanes; still bit-identical to one
+    lane and within tolerance of the oracle."""
+    g = 130
+    m = pk.make_heat3d(g)
+    n = g ** 3
+    rng = np.random.default_rng(41)
+    lo = rng.uniform(0.5, 1.0, n)
+    hi = lo + rng.uniform(0.0, 0.5, n)
+    h = 0.2 / (g - 1) ** 2
+    prob = pk.ReachProblem(m, pk.IntervalVector(lo, hi), None, 0.0, 3 * h + 1e-7 * h, h, 1)
+    c1, ck = lanes_ctx(1, "fast"), lanes_ctx(3, "fast")
+    try:
+        a = pk.mixed_monotonicity(prob, ctx=c1)
+        same(a, pk.mixed_monotonicity(prob, ctx=ck))
+        assert_within(a, oracle_mm(prob))
+    finally:
+        c1.close()
+        ck.close()
+
+
 def test_workers_argument_maps_to_lanes():
     """The reference's `workers` (reach.hpp:53) selects the lane count: the
     package's process-wide worker contexts, bit-identical results."""
