@@ -325,6 +325,15 @@ SmallModel small_model(const pirk_model* m) {
     s.grid = m->grid;
     for (int i = 0; i < 8; ++i) s.P[i] = m->params[i];
     s.has_C = growth_matrix(m, s.C) ? 1 : 0;
+    if (m->kind == PIRK_ARCH_QUAD) {  // uniform divisions hoisted out of every RHS evaluation
+        const double mass = m->params[0], jx = m->params[2], jy = m->params[3], jz = m->params[4];
+        s.Q[0] = (jy - jz) / jx;
+        s.Q[1] = (jz - jx) / jy;
+        s.Q[2] = (jx - jy) / jz;
+        s.Q[3] = 1.0 / jx;
+        s.Q[4] = 1.0 / jy;
+        s.Q[5] = 1.0 / mass;
+    }
     return s;
 }
 

@@ -75,6 +75,10 @@ struct SmallModel {
     double P[8];
     int has_C;
     double C[12 * 12];  // dense growth matrix (row-major n x n) for n <= 12
+    // host-derived constants, each the same IEEE operation the device would do
+    // per evaluation (arch-quadrotor: (jy-jz)/jx, (jz-jx)/jy, (jx-jy)/jz, 1/jx,
+    // 1/jy, 1/mass; models.cpp:520-552)
+    double Q[8];
 };
 
 template <bool Exact>

@@ -91,8 +91,8 @@ static __device__ double sm_f(const SmallModel& m, int i, const double* x, const
 // arch-quadrotor, all 12 components with the trig evaluated once (the
 // reference recomputes identical values per component, models.cpp:522-524).
 __device__ __forceinline__ void aq_f_all(const SmallModel& m, const double* x, double* f) {
-    const double mass = m.P[0], gravity = m.P[1], jx = m.P[2], jy = m.P[3], jz = m.P[4];
-    const double kx = (jy - jz) / jx, ky = (jz - jx) / jy, kz = (jx - jy) / jz;
+    const double mass = m.P[0], gravity = m.P[1], jx = m.P[2], jy = m.P[3];
+    const double kx = m.Q[0], ky = m.Q[1], kz = m.Q[2];  // (jy - jz) / jx, ... (host, same IEEE division)
     double s7, c7, s8, c8, s9, c9;
     sincos(x[6], &s7, &c7);
     sincos(x[7], &s8, &c8);
@@ -157,9 +157,9 @@ __device__ __forceinline__ void small_sincos(double x, double* s, double* c) {
 // and the constant quotients folded (tolerance-only in both modes: glibc and
 // CUDA trig differ in the last ulp, DESIGN.md (c))
 __device__ __forceinline__ void aq_f_all_fast(const SmallModel& m, const double* x, double* f) {
-    const double mass = m.P[0], gravity = m.P[1], jx = m.P[2], jy = m.P[3], jz = m.P[4];
-    const double kx = (jy - jz) / jx, ky = (jz - jx) / jy, kz = (jx - jy) / jz;  // uniform: hoisted
-    const double ijx = 1.0 / jx, ijy = 1.0 / jy, imass = 1.0 / mass;
+    const double mass = m.P[0], gravity = m.P[1];
+    const double kx = m.Q[0], ky = m.Q[1], kz = m.Q[2];  // uniform divisions, computed on the host
+    const double ijx = m.Q[3], ijy = m.Q[4], imass = m.Q[5];
     double s7, c7, s8, c8, s9, c9;
     small_sincos(x[6], &s7, &c7);
     small_sincos(x[7], &s8, &c8);
