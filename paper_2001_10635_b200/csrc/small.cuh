@@ -164,7 +164,18 @@ __device__ __forceinline__ void aq_f_all_fast(const SmallModel& m, const double*
     small_sincos(x[6], &s7, &c7);
     small_sincos(x[7], &s8, &c8);
     small_sincos(x[8], &s9, &c9);
-    const double ic8 = 1.0 / c8, t8 = s8 * ic8;
+    // 1/c8: hardware reciprocal estimate + two Newton steps (~1 ulp; fast mode),
+    // without the division's special-case branch (c8 = cos(theta) is nonzero on
+    // the model's operating box)
+    double ic8;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(ic8) : "d"(c8));
+    {
+        double e = fma(-c8, ic8, 1.0);
+        ic8 = fma(ic8, e, ic8);
+        e = fma(-c8, ic8, 1.0);
+        ic8 = fma(ic8, e, ic8);
+    }
+    const double t8 = s8 * ic8;
     f[0] = c8 * c9 * x[3] + (s7 * s8 * c9 - c7 * s9) * x[4] + (c7 * s8 * c9 + s7 * s9) * x[5];
     f[1] = c8 * s9 * x[3] + (s7 * s8 * s9 + c7 * c9) * x[4] + (c7 * s8 * s9 - s7 * c9) * x[5];
     f[2] = s8 * x[3] - s7 * c8 * x[4] - c7 * c8 * x[5];
